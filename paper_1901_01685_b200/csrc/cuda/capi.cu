@@ -1,0 +1,982 @@
+// C ABI of libpmg_cuda.so (include/pmg_cuda.h): device handles, the p-multigrid
+// hierarchy and the V-cycle / solve drivers.  Every floating-point operation of the
+// solve runs in the kernels of sell.cu / trsv.cu / dense.cu; the host only sequences
+// launches on the work stream.
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../../include/pmg_cuda.h"
+#include "dense.cuh"
+#include "ilut.cuh"
+#include "rcm.hpp"
+#include "sell.cuh"
+#include "trsv.cuh"
+
+using namespace pmg;
+
+namespace {
+thread_local std::string g_err;
+
+struct ArgError : std::runtime_error {
+    int status;
+    ArgError(const std::string& m, int s) : std::runtime_error(m), status(s) {}
+};
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        return f();
+    } catch (const CudaError& e) {
+        g_err = e.what();
+        return e.status;
+    } catch (const ArgError& e) {
+        g_err = e.what();
+        return e.status;
+    } catch (const std::bad_alloc& e) {
+        g_err = "host allocation failed";
+        return PMG_ERR_OOM;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return PMG_ERR_CUDA;
+    }
+}
+
+void check_view(const pmg_csr_view* v) {
+    if (!v || v->nrows < 0 || v->ncols < 0 || !v->rowptr) throw ArgError("null/invalid CSR view", PMG_ERR_ARG);
+    if (v->rowptr[0] != 0) throw ArgError("CSR rowptr[0] != 0", PMG_ERR_ARG);
+    for (int32_t i = 0; i < v->nrows; ++i) {
+        if (v->rowptr[i + 1] < v->rowptr[i]) throw ArgError("CSR rowptr decreasing", PMG_ERR_ARG);
+        for (int32_t k = v->rowptr[i]; k < v->rowptr[i + 1]; ++k) {
+            if (v->col[k] < 0 || v->col[k] >= v->ncols) throw ArgError("CSR column out of range", PMG_ERR_ARG);
+            if (k > v->rowptr[i] && v->col[k] <= v->col[k - 1])
+                throw ArgError("CSR columns not strictly increasing", PMG_ERR_ARG);
+        }
+    }
+}
+
+template <class T>
+T* dalloc(size_t n) {
+    T* p = nullptr;
+    PMG_CUDA(cudaMalloc(&p, sizeof(T) * std::max<size_t>(n, 1)));
+    return p;
+}
+
+DevCsr upload(const pmg_csr_view& v, cudaStream_t st) {
+    DevCsr d;
+    d.n = v.nrows;
+    d.m = v.ncols;
+    d.nnz = v.rowptr[v.nrows];
+    d.rowptr = dalloc<int32_t>(v.nrows + 1);
+    d.col = dalloc<int32_t>(d.nnz);
+    d.val = dalloc<double>(d.nnz);
+    PMG_CUDA(cudaMemcpyAsync(d.rowptr, v.rowptr, sizeof(int32_t) * (v.nrows + 1), cudaMemcpyHostToDevice, st));
+    if (d.nnz) {
+        PMG_CUDA(cudaMemcpyAsync(d.col, v.col, sizeof(int32_t) * d.nnz, cudaMemcpyHostToDevice, st));
+        PMG_CUDA(cudaMemcpyAsync(d.val, v.val, sizeof(double) * d.nnz, cudaMemcpyHostToDevice, st));
+    }
+    return d;
+}
+
+struct Stream {
+    cudaStream_t s = nullptr;
+    Stream() { PMG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)); }
+    ~Stream() {
+        if (s) cudaStreamDestroy(s);
+    }
+};
+
+}  // namespace
+
+// =================================================================== handles
+struct pmg_csr_s {
+    DevCsr A;
+    Sell S;                       // identity-order sliced layout (SpMV family)
+    std::vector<int32_t> h_rowptr, h_col;
+    std::vector<double> h_val;    // host copy (setup: RCM / permutation)
+    int32_t band = 0;
+    // Gauss-Seidel structures (built on first use)
+    bool gs_ready = false;
+    int64_t gs_zero_row = -1;
+    LevelSets gs_lv;
+    Sell gs;
+    double* gs_diag = nullptr;
+    int32_t* gs_nlow = nullptr;
+    ~pmg_csr_s() {
+        A.free();
+        sell_free(S);
+        if (gs_ready) {
+            level_sets_free(gs_lv);
+            sell_free(gs);
+            cudaFree(gs_diag);
+            cudaFree(gs_nlow);
+        }
+    }
+};
+
+struct pmg_factor_s {
+    int32_t n = 0;
+    DevCsr L, U;
+    int32_t* perm = nullptr;          // device, null for the identity ordering
+    std::vector<int32_t> h_perm;
+    LevelSets lvL, lvU;
+    Sell Ls, Us;
+    double* Udiag = nullptr;          // diagonal of U per U-level position
+    int32_t max_row_L = 0, max_row_U = 0;
+    double seconds = 0;
+    ~pmg_factor_s() {
+        L.free();
+        U.free();
+        cudaFree(perm);
+        level_sets_free(lvL);
+        level_sets_free(lvU);
+        sell_free(Ls);
+        sell_free(Us);
+        cudaFree(Udiag);
+    }
+};
+
+namespace {
+
+pmg_csr_s* make_csr(const pmg_csr_view& v, cudaStream_t st) {
+    auto h = std::make_unique<pmg_csr_s>();
+    h->A = upload(v, st);
+    h->h_rowptr.assign(v.rowptr, v.rowptr + v.nrows + 1);
+    h->h_col.assign(v.col, v.col + h->A.nnz);
+    h->h_val.assign(v.val, v.val + h->A.nnz);
+    h->band = pmg_host::bandwidth(v.nrows, v.rowptr, v.col);
+    sell_build(h->S, v.nrows, h->A.rowptr, h->A.col, h->A.val, nullptr, kPickAll, nullptr, nullptr, st);
+    PMG_CUDA(cudaStreamSynchronize(st));
+    return h.release();
+}
+
+void ensure_gs(pmg_csr_s* h, cudaStream_t st) {
+    if (h->gs_ready) return;
+    const int32_t n = h->A.n;
+    level_sets(h->gs_lv, n, h->A.rowptr, h->A.col, kDepLower, st);
+    h->gs_diag = dalloc<double>(n);
+    h->gs_nlow = dalloc<int32_t>(n);
+    sell_build(h->gs, n, h->A.rowptr, h->A.col, h->A.val, h->gs_lv.order, kPickOffDiag, h->gs_diag, h->gs_nlow, st);
+    // first row (in row order) with a zero or missing diagonal -> SPEC.md:237 smoother error
+    std::vector<double> dg(n);
+    std::vector<int32_t> ord(n);
+    PMG_CUDA(cudaMemcpyAsync(dg.data(), h->gs_diag, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    PMG_CUDA(cudaMemcpyAsync(ord.data(), h->gs_lv.order, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
+    PMG_CUDA(cudaStreamSynchronize(st));
+    int64_t zr = -1;
+    for (int32_t p = 0; p < n; ++p)
+        if (dg[p] == 0.0 && (zr < 0 || ord[p] < zr)) zr = ord[p];
+    h->gs_zero_row = zr;
+    h->gs_ready = true;
+}
+
+// ILUT of csr under `ordering`; on zero pivot returns PMG_ZERO_PIVOT with *err_row
+int make_factor(pmg_csr_s* A, double tau, double fillfactor, int ordering, pmg_factor_s** out, int64_t* err_row,
+                cudaStream_t st) {
+    if (A->A.n != A->A.m) throw ArgError("ilut: matrix not square", PMG_ERR_DIM);
+    if (!(tau >= 0) || !(fillfactor >= 1)) throw ArgError("ilut: tau >= 0 and fillfactor >= 1 required", PMG_ERR_ARG);
+    auto F = std::make_unique<pmg_factor_s>();
+    const int32_t n = A->A.n;
+    F->n = n;
+    DevCsr Ap = A->A;
+    DevCsr owned;
+    int32_t band = A->band;
+    if (ordering == PMG_ORDER_RCM) {
+        F->h_perm = pmg_host::rcm_ordering(n, A->h_rowptr.data(), A->h_col.data());
+        std::vector<int32_t> brp, bci;
+        std::vector<double> bv;
+        band = pmg_host::permute_symmetric(n, A->h_rowptr.data(), A->h_col.data(), A->h_val.data(), F->h_perm, brp,
+                                           bci, bv);
+        pmg_csr_view v{n, n, brp.data(), bci.data(), bv.data()};
+        owned = upload(v, st);
+        Ap = owned;
+        F->perm = dalloc<int32_t>(n);
+        PMG_CUDA(cudaMemcpyAsync(F->perm, F->h_perm.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, st));
+        PMG_CUDA(cudaStreamSynchronize(st));
+    } else if (ordering != PMG_ORDER_NONE) {
+        throw ArgError("unknown ordering", PMG_ERR_ARG);
+    }
+    int rc = ilut_factorize_device(Ap, band, tau, fillfactor, F->L, F->U, err_row, &F->seconds, st);
+    owned.free();
+    if (rc != 0) return PMG_ZERO_PIVOT;
+    level_sets(F->lvL, n, F->L.rowptr, F->L.col, kDepLower, st);
+    level_sets(F->lvU, n, F->U.rowptr, F->U.col, kDepUpper, st);
+    sell_build(F->Ls, n, F->L.rowptr, F->L.col, F->L.val, F->lvL.order, kPickAll, nullptr, nullptr, st);
+    F->Udiag = dalloc<double>(n);
+    sell_build(F->Us, n, F->U.rowptr, F->U.col, F->U.val, F->lvU.order, kPickOffDiagDesc, F->Udiag, nullptr, st);
+    // longest rows (reporting)
+    std::vector<int32_t> lr(n + 1), ur(n + 1);
+    PMG_CUDA(cudaMemcpyAsync(lr.data(), F->L.rowptr, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToHost, st));
+    PMG_CUDA(cudaMemcpyAsync(ur.data(), F->U.rowptr, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToHost, st));
+    PMG_CUDA(cudaStreamSynchronize(st));
+    for (int32_t i = 0; i < n; ++i) {
+        F->max_row_L = std::max(F->max_row_L, lr[i + 1] - lr[i]);
+        F->max_row_U = std::max(F->max_row_U, ur[i + 1] - ur[i]);
+    }
+    *out = F.release();
+    return PMG_OK;
+}
+
+}  // namespace
+
+// =================================================================== hierarchy
+namespace {
+
+struct PLev {
+    int degree = 1;
+    pmg_csr_s* A = nullptr;
+    pmg_csr_s* P = nullptr;   // level l+1 -> l (rows of this level)
+    pmg_csr_s* PT = nullptr;
+    double* ML = nullptr;
+    pmg_factor_s* F = nullptr;
+};
+struct HLev {
+    pmg_csr_s* A = nullptr;   // for j = 0: alias of the last p-level's A
+    bool own_A = false;
+    pmg_csr_s* P = nullptr;
+    pmg_csr_s* PT = nullptr;
+    pmg_factor_s* F = nullptr;
+};
+
+}  // namespace
+
+struct pmg_hier_s {
+    std::vector<PLev> pl;
+    std::vector<HLev> hl;
+    DenseLU coarse;
+    int smoother = PMG_SMOOTHER_ILUT, nu1 = 1, nu2 = 1;
+    pmg_hier_stats stats{};
+    ~pmg_hier_s() {
+        for (auto& l : pl) {
+            delete l.A;
+            delete l.P;
+            delete l.PT;
+            cudaFree(l.ML);
+            delete l.F;
+        }
+        for (auto& h : hl) {
+            if (h.own_A) delete h.A;
+            delete h.P;
+            delete h.PT;
+            delete h.F;
+        }
+        dense_free(coarse);
+    }
+};
+
+// -------------------------------------------------------------------- work / cycle
+namespace {
+
+enum Cls { kClsResid0 = 0, kClsL0, kClsU0, kClsGS0, kClsTransfer, kClsCoarse, kClsMisc, kNumCls };
+
+struct PWork {
+    double* u[2] = {nullptr, nullptr};
+    int cur = 0;
+    double *f = nullptr, *r = nullptr, *y = nullptr, *x = nullptr;
+};
+struct HWork {
+    double *e = nullptr, *r = nullptr, *res = nullptr, *y = nullptr, *x = nullptr;
+};
+
+}  // namespace
+
+struct pmg_work_s {
+    pmg_hier_s* H = nullptr;
+    cudaStream_t st = nullptr;
+    std::vector<PWork> pw;
+    std::vector<HWork> hw;
+    int* ticket = nullptr;
+    NormCtx nc{};
+    double* norm0 = nullptr;
+    double* dhist = nullptr;
+    int hist_cap = 0;
+    double* h_pinned = nullptr;
+    // optional per-class event timing
+    bool prof = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool;
+    std::vector<int> ev_cls;
+    size_t ev_used = 0;
+    double cls_ms[kNumCls] = {};
+    int64_t launches = 0;
+    int64_t cls_launches[kNumCls] = {};
+
+    ~pmg_work_s() {
+        for (auto& p : pw) {
+            cudaFree(p.u[0]);
+            cudaFree(p.u[1]);
+            cudaFree(p.f);
+            cudaFree(p.r);
+            cudaFree(p.y);
+            cudaFree(p.x);
+        }
+        for (auto& h : hw) {
+            cudaFree(h.e);
+            cudaFree(h.r);
+            cudaFree(h.res);
+            cudaFree(h.y);
+            cudaFree(h.x);
+        }
+        cudaFree(ticket);
+        cudaFree(nc.partials);
+        cudaFree(nc.counter);
+        cudaFree(norm0);
+        cudaFree(dhist);
+        cudaFreeHost(h_pinned);
+        for (auto& e : ev_pool) {
+            cudaEventDestroy(e.first);
+            cudaEventDestroy(e.second);
+        }
+        if (st) cudaStreamDestroy(st);
+    }
+
+    template <class F>
+    void run(int cls, int nlaunch, F&& f) {
+        launches += nlaunch;
+        cls_launches[cls] += nlaunch;
+        if (!prof) {
+            f();
+            return;
+        }
+        if (ev_used == ev_pool.size()) {
+            cudaEvent_t a, b;
+            PMG_CUDA(cudaEventCreate(&a));
+            PMG_CUDA(cudaEventCreate(&b));
+            ev_pool.push_back({a, b});
+            ev_cls.push_back(0);
+        }
+        auto& e = ev_pool[ev_used];
+        ev_cls[ev_used] = cls;
+        ++ev_used;
+        PMG_CUDA(cudaEventRecord(e.first, st));
+        f();
+        PMG_CUDA(cudaEventRecord(e.second, st));
+    }
+    void collect() {
+        if (!prof || ev_used == 0) return;
+        PMG_CUDA(cudaStreamSynchronize(st));
+        for (size_t k = 0; k < ev_used; ++k) {
+            float ms = 0;
+            PMG_CUDA(cudaEventElapsedTime(&ms, ev_pool[k].first, ev_pool[k].second));
+            cls_ms[ev_cls[k]] += ms;
+        }
+        ev_used = 0;
+    }
+};
+
+namespace {
+
+void smooth_ilut(pmg_work_s& W, pmg_csr_s* A, pmg_factor_s* F, double* u, const double* f, const double* r_known,
+                 double* r, double* y, double* x, bool fine) {
+    const double* rr = r_known;
+    if (!rr) {
+        W.run(fine ? kClsResid0 : kClsCoarse, 1, [&] { sell_rowop(A->S, kOpResidual, u, f, nullptr, r, nullptr, W.st); });
+        rr = r;
+    }
+    W.run(fine ? kClsL0 : kClsCoarse, 3, [&] { lsolve(F->Ls, F->perm, rr, y, W.ticket, W.st); });
+    W.run(fine ? kClsU0 : kClsCoarse, 3, [&] { usolve_add(F->Us, F->Udiag, F->perm, y, x, u, W.ticket, W.st); });
+}
+
+// one h-MG V(1,1) cycle on h-level j from e = 0
+void hmg(pmg_work_s& W, int j, double* e, const double* r) {
+    pmg_hier_s& H = *W.H;
+    HLev& L = H.hl[j];
+    HWork& w = W.hw[j];
+    const int32_t n = L.A->A.n;
+    if (j == int(H.hl.size()) - 1) {
+        W.run(kClsCoarse, 1, [&] { dense_solve(H.coarse, r, e, W.st); });
+        return;
+    }
+    W.run(kClsCoarse, 0, [&] { PMG_CUDA(cudaMemsetAsync(e, 0, sizeof(double) * n, W.st)); });
+    smooth_ilut(W, L.A, L.F, e, r, r, nullptr, w.y, w.x, false);
+    W.run(kClsCoarse, 1, [&] { sell_rowop(L.A->S, kOpResidual, e, r, nullptr, w.res, nullptr, W.st); });
+    HWork& c = W.hw[j + 1];
+    W.run(kClsCoarse, 1, [&] { sell_rowop(L.PT->S, kOpSpmv, w.res, nullptr, nullptr, c.r, nullptr, W.st); });
+    hmg(W, j + 1, c.e, c.r);
+    W.run(kClsCoarse, 1, [&] { sell_rowop(L.P->S, kOpAdd, c.e, nullptr, nullptr, e, nullptr, W.st); });
+    smooth_ilut(W, L.A, L.F, e, r, nullptr, w.res, w.y, w.x, false);
+}
+
+int smooth(pmg_work_s& W, int l, const double* f, const double* r_known) {
+    pmg_hier_s& H = *W.H;
+    PLev& L = H.pl[l];
+    PWork& w = W.pw[l];
+    const bool fine = l == 0;
+    if (H.smoother == PMG_SMOOTHER_GS) {
+        if (L.A->gs_zero_row >= 0) return PMG_ZERO_DIAG;
+        double* uo = w.u[w.cur];
+        double* un = w.u[1 - w.cur];
+        W.run(fine ? kClsGS0 : kClsCoarse, 3, [&] {
+            gs_sweep(L.A->gs, L.A->gs_diag, L.A->gs_nlow, f, uo, un, W.ticket, W.st);
+        });
+        w.cur = 1 - w.cur;
+        return PMG_OK;
+    }
+    smooth_ilut(W, L.A, L.F, w.u[w.cur], f, r_known, w.r, w.y, w.x, fine);
+    return PMG_OK;
+}
+
+// V-cycle at p-level l; `zero`: u == 0 on entry (its residual is f)
+int vcycle(pmg_work_s& W, int l, const double* f, const double* r_known, bool zero) {
+    pmg_hier_s& H = *W.H;
+    PWork& w = W.pw[l];
+    if (l == int(H.pl.size()) - 1) {
+        hmg(W, 0, w.u[w.cur], f);
+        return PMG_OK;
+    }
+    PLev& L = H.pl[l];
+    const bool fine = l == 0;
+    for (int s = 0; s < H.nu1; ++s) {
+        int rc = smooth(W, l, f, s == 0 ? (zero ? f : r_known) : nullptr);
+        if (rc) return rc;
+    }
+    W.run(fine ? kClsResid0 : kClsCoarse, 1,
+          [&] { sell_rowop(L.A->S, kOpResidual, w.u[w.cur], f, nullptr, w.r, nullptr, W.st); });
+    PLev& C = H.pl[l + 1];
+    PWork& c = W.pw[l + 1];
+    W.run(fine ? kClsTransfer : kClsCoarse, 1,
+          [&] { sell_rowop(L.PT->S, kOpRestrict, w.r, nullptr, C.ML, c.f, nullptr, W.st); });
+    W.run(kClsCoarse, 0, [&] { PMG_CUDA(cudaMemsetAsync(c.u[c.cur], 0, sizeof(double) * C.A->A.n, W.st)); });
+    int rc = vcycle(W, l + 1, c.f, nullptr, true);
+    if (rc) return rc;
+    W.run(fine ? kClsTransfer : kClsCoarse, 1,
+          [&] { sell_rowop(L.P->S, kOpProlongAdd, c.u[c.cur], nullptr, L.ML, w.u[w.cur], nullptr, W.st); });
+    for (int s = 0; s < H.nu2; ++s) {
+        rc = smooth(W, l, f, nullptr);
+        if (rc) return rc;
+    }
+    return PMG_OK;
+}
+
+void ensure_hist(pmg_work_s& W, int max_cycles) {
+    if (W.hist_cap >= max_cycles + 1) return;
+    cudaFree(W.dhist);
+    cudaFreeHost(W.h_pinned);
+    W.dhist = dalloc<double>(max_cycles + 1);
+    PMG_CUDA(cudaMallocHost(&W.h_pinned, sizeof(double) * (max_cycles + 1)));
+    W.hist_cap = max_cycles + 1;
+}
+
+// the solve loop on device-resident f / u (u = pw[0].u[cur] on entry and exit)
+int solve_loop(pmg_work_s& W, const double* d_f, double tol, int max_cycles, double* rho_hist, int* cycles, int* flags,
+               double* seconds) {
+    pmg_hier_s& H = *W.H;
+    PLev& L0 = H.pl[0];
+    PWork& w0 = W.pw[0];
+    const int32_t n = L0.A->A.n;
+    ensure_hist(W, max_cycles);
+    cudaEvent_t e0, e1;
+    PMG_CUDA(cudaEventCreate(&e0));
+    PMG_CUDA(cudaEventCreate(&e1));
+    PMG_CUDA(cudaEventRecord(e0, W.st));
+    NormCtx nc = W.nc;
+    nc.norm_out = W.norm0;
+    nc.n0 = nullptr;
+    nc.hist_out = nullptr;
+    W.run(kClsResid0, 1, [&] { sell_rowop(L0.A->S, kOpResidual, w0.u[w0.cur], d_f, nullptr, w0.r, &nc, W.st); });
+    PMG_CUDA(cudaMemcpyAsync(W.h_pinned, W.norm0, sizeof(double), cudaMemcpyDeviceToHost, W.st));
+    PMG_CUDA(cudaStreamSynchronize(W.st));
+    const double n0 = W.h_pinned[0];
+    rho_hist[0] = 1.0;
+    *cycles = 0;
+    *flags = 0;
+    int rc = PMG_OK;
+    if (n0 == 0.0) {
+        *flags = PMG_FLAG_CONVERGED;
+    } else {
+        for (int c = 1; c <= max_cycles; ++c) {
+            rc = vcycle(W, 0, d_f, w0.r, false);
+            if (rc) break;
+            NormCtx ncc = W.nc;
+            ncc.norm_out = nullptr;
+            ncc.n0 = W.norm0;
+            ncc.hist_out = W.dhist + c;
+            W.run(kClsResid0, 1,
+                  [&] { sell_rowop(L0.A->S, kOpResidual, w0.u[w0.cur], d_f, nullptr, w0.r, &ncc, W.st); });
+            PMG_CUDA(cudaMemcpyAsync(W.h_pinned + c, W.dhist + c, sizeof(double), cudaMemcpyDeviceToHost, W.st));
+            PMG_CUDA(cudaStreamSynchronize(W.st));
+            const double rho = W.h_pinned[c];
+            rho_hist[c] = rho;
+            *cycles = c;
+            if (rho <= tol) {
+                *flags = PMG_FLAG_CONVERGED;
+                break;
+            }
+            if (!(rho <= 1e10)) {
+                *flags = PMG_FLAG_DIVERGED;
+                break;
+            }
+        }
+    }
+    PMG_CUDA(cudaEventRecord(e1, W.st));
+    PMG_CUDA(cudaEventSynchronize(e1));
+    float ms = 0;
+    PMG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    if (seconds) *seconds = ms * 1e-3;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    W.collect();
+    (void)n;
+    return rc;
+}
+
+}  // namespace
+
+// =================================================================== C ABI
+extern "C" {
+
+const char* pmg_status_string(int s) {
+    switch (s) {
+        case PMG_OK: return "ok";
+        case PMG_ZERO_PIVOT: return "zero pivot";
+        case PMG_ZERO_DIAG: return "zero diagonal";
+        case PMG_ERR_DIM: return "dimension mismatch";
+        case PMG_ERR_CUDA: return "cuda error";
+        case PMG_ERR_OOM: return "out of memory";
+        case PMG_ERR_ARG: return "invalid argument";
+    }
+    return "unknown";
+}
+
+const char* pmg_last_error(void) { return g_err.c_str(); }
+
+int pmg_device_info(int* sm_count, int* cc_major, int* cc_minor) {
+    return guarded([&] {
+        int dev = 0;
+        PMG_CUDA(cudaGetDevice(&dev));
+        cudaDeviceProp p;
+        PMG_CUDA(cudaGetDeviceProperties(&p, dev));
+        if (sm_count) *sm_count = p.multiProcessorCount;
+        if (cc_major) *cc_major = p.major;
+        if (cc_minor) *cc_minor = p.minor;
+        return PMG_OK;
+    });
+}
+
+int pmg_csr_create(const pmg_csr_view* A, pmg_csr* out) {
+    return guarded([&] {
+        check_view(A);
+        Stream s;
+        *out = make_csr(*A, s.s);
+        return PMG_OK;
+    });
+}
+
+int pmg_csr_destroy(pmg_csr A) {
+    delete A;
+    return PMG_OK;
+}
+
+namespace {
+struct HostVecs {
+    std::vector<double*> ptrs;
+    ~HostVecs() {
+        for (auto p : ptrs) cudaFree(p);
+    }
+    double* make(size_t n) {
+        ptrs.push_back(dalloc<double>(n));
+        return ptrs.back();
+    }
+};
+}  // namespace
+
+int pmg_spmv(pmg_csr A, const double* x, double* y) {
+    return guarded([&] {
+        Stream s;
+        HostVecs hv;
+        double* dx = hv.make(A->A.m);
+        double* dy = hv.make(A->A.n);
+        PMG_CUDA(cudaMemcpyAsync(dx, x, sizeof(double) * A->A.m, cudaMemcpyHostToDevice, s.s));
+        sell_rowop(A->S, kOpSpmv, dx, nullptr, nullptr, dy, nullptr, s.s);
+        PMG_CUDA(cudaMemcpyAsync(y, dy, sizeof(double) * A->A.n, cudaMemcpyDeviceToHost, s.s));
+        PMG_CUDA(cudaStreamSynchronize(s.s));
+        return PMG_OK;
+    });
+}
+
+int pmg_residual(pmg_csr A, const double* x, const double* f, double* r, double* norm2) {
+    return guarded([&] {
+        Stream s;
+        HostVecs hv;
+        const int32_t n = A->A.n;
+        double* dx = hv.make(A->A.m);
+        double* df = hv.make(n);
+        double* dr = hv.make(n);
+        double* parts = hv.make(ceil_div(n, 256) + 1);
+        double* nrm = hv.make(1);
+        unsigned* cnt = reinterpret_cast<unsigned*>(hv.make(1));
+        PMG_CUDA(cudaMemsetAsync(cnt, 0, sizeof(double), s.s));
+        PMG_CUDA(cudaMemcpyAsync(dx, x, sizeof(double) * A->A.m, cudaMemcpyHostToDevice, s.s));
+        PMG_CUDA(cudaMemcpyAsync(df, f, sizeof(double) * n, cudaMemcpyHostToDevice, s.s));
+        NormCtx nc{parts, cnt, nrm, nullptr, nullptr};
+        sell_rowop(A->S, kOpResidual, dx, df, nullptr, dr, &nc, s.s);
+        PMG_CUDA(cudaMemcpyAsync(r, dr, sizeof(double) * n, cudaMemcpyDeviceToHost, s.s));
+        if (norm2) PMG_CUDA(cudaMemcpyAsync(norm2, nrm, sizeof(double), cudaMemcpyDeviceToHost, s.s));
+        PMG_CUDA(cudaStreamSynchronize(s.s));
+        return PMG_OK;
+    });
+}
+
+int pmg_gs_sweep(pmg_csr A, double* u, const double* f, int64_t* err_row) {
+    return guarded([&] {
+        if (A->A.n != A->A.m) throw ArgError("gs: matrix not square", PMG_ERR_DIM);
+        Stream s;
+        ensure_gs(A, s.s);
+        if (A->gs_zero_row >= 0) {
+            if (err_row) *err_row = A->gs_zero_row;
+            return int(PMG_ZERO_DIAG);
+        }
+        HostVecs hv;
+        const int32_t n = A->A.n;
+        double* du = hv.make(n);
+        double* dn = hv.make(n);
+        double* df = hv.make(n);
+        int* tk = reinterpret_cast<int*>(hv.make(1));
+        PMG_CUDA(cudaMemcpyAsync(du, u, sizeof(double) * n, cudaMemcpyHostToDevice, s.s));
+        PMG_CUDA(cudaMemcpyAsync(df, f, sizeof(double) * n, cudaMemcpyHostToDevice, s.s));
+        gs_sweep(A->gs, A->gs_diag, A->gs_nlow, df, du, dn, tk, s.s);
+        PMG_CUDA(cudaMemcpyAsync(u, dn, sizeof(double) * n, cudaMemcpyDeviceToHost, s.s));
+        PMG_CUDA(cudaStreamSynchronize(s.s));
+        return int(PMG_OK);
+    });
+}
+
+int pmg_rcm_ordering(const pmg_csr_view* A, int32_t* perm) {
+    return guarded([&] {
+        check_view(A);
+        auto p = pmg_host::rcm_ordering(A->nrows, A->rowptr, A->col);
+        std::copy(p.begin(), p.end(), perm);
+        return PMG_OK;
+    });
+}
+
+int pmg_ilut_factorize(pmg_csr A, double tau, double fillfactor, int ordering, pmg_factor* out, int64_t* err_row) {
+    return guarded([&] {
+        Stream s;
+        return make_factor(A, tau, fillfactor, ordering, out, err_row, s.s);
+    });
+}
+
+int pmg_factor_destroy(pmg_factor F) {
+    delete F;
+    return PMG_OK;
+}
+
+int pmg_ilut_apply(pmg_factor F, const double* r, double* e) {
+    return guarded([&] {
+        Stream s;
+        HostVecs hv;
+        const int32_t n = F->n;
+        double* dr = hv.make(n);
+        double* dy = hv.make(n);
+        double* dx = hv.make(n);
+        double* de = hv.make(n);
+        int* tk = reinterpret_cast<int*>(hv.make(1));
+        PMG_CUDA(cudaMemcpyAsync(dr, r, sizeof(double) * n, cudaMemcpyHostToDevice, s.s));
+        PMG_CUDA(cudaMemsetAsync(de, 0, sizeof(double) * n, s.s));
+        lsolve(F->Ls, F->perm, dr, dy, tk, s.s);
+        usolve_add(F->Us, F->Udiag, F->perm, dy, dx, de, tk, s.s);
+        PMG_CUDA(cudaMemcpyAsync(e, de, sizeof(double) * n, cudaMemcpyDeviceToHost, s.s));
+        PMG_CUDA(cudaStreamSynchronize(s.s));
+        return PMG_OK;
+    });
+}
+
+int pmg_factor_stats(pmg_factor F, int64_t* nnz_L, int64_t* nnz_U, int32_t* levels_L, int32_t* levels_U,
+                     int32_t* max_row_L, int32_t* max_row_U) {
+    if (nnz_L) *nnz_L = F->L.nnz;
+    if (nnz_U) *nnz_U = F->U.nnz;
+    if (levels_L) *levels_L = F->lvL.nlevels;
+    if (levels_U) *levels_U = F->lvU.nlevels;
+    if (max_row_L) *max_row_L = F->max_row_L;
+    if (max_row_U) *max_row_U = F->max_row_U;
+    return PMG_OK;
+}
+
+int pmg_factor_export(pmg_factor F, int32_t* Lrp, int32_t* Lc, double* Lv, int32_t* Urp, int32_t* Uc, double* Uv,
+                      int32_t* perm) {
+    return guarded([&] {
+        const int32_t n = F->n;
+        auto cp = [](void* dst, const void* src, size_t bytes) {
+            if (dst && bytes) PMG_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+        };
+        cp(Lrp, F->L.rowptr, sizeof(int32_t) * (n + 1));
+        cp(Lc, F->L.col, sizeof(int32_t) * F->L.nnz);
+        cp(Lv, F->L.val, sizeof(double) * F->L.nnz);
+        cp(Urp, F->U.rowptr, sizeof(int32_t) * (n + 1));
+        cp(Uc, F->U.col, sizeof(int32_t) * F->U.nnz);
+        cp(Uv, F->U.val, sizeof(double) * F->U.nnz);
+        if (perm) {
+            if (F->h_perm.empty())
+                for (int32_t i = 0; i < n; ++i) perm[i] = i;
+            else
+                std::copy(F->h_perm.begin(), F->h_perm.end(), perm);
+        }
+        return PMG_OK;
+    });
+}
+
+int pmg_hier_create(const pmg_hier_desc* d, pmg_hier* out, int* err_level, int64_t* err_row) {
+    return guarded([&] {
+        auto t0 = std::chrono::steady_clock::now();
+        if (!d || d->n_plevels < 1 || d->n_hlevels < 1) throw ArgError("hierarchy: need >= 1 p- and h-level", PMG_ERR_ARG);
+        if (d->degrees[d->n_plevels - 1] != 1) throw ArgError("hierarchy: last p-level must have degree 1", PMG_ERR_ARG);
+        if (d->nu1 < 0 || d->nu2 < 0) throw ArgError("hierarchy: nu1, nu2 >= 0", PMG_ERR_ARG);
+        Stream s;
+        auto H = std::make_unique<pmg_hier_s>();
+        H->smoother = d->smoother;
+        H->nu1 = d->nu1;
+        H->nu2 = d->nu2;
+        const int np = d->n_plevels, nh = d->n_hlevels;
+        H->pl.resize(np);
+        for (int l = 0; l < np; ++l) {
+            check_view(&d->A[l]);
+            PLev& L = H->pl[l];
+            L.degree = d->degrees[l];
+            L.A = make_csr(d->A[l], s.s);
+            L.ML = dalloc<double>(L.A->A.n);
+            PMG_CUDA(cudaMemcpyAsync(L.ML, d->ML[l], sizeof(double) * L.A->A.n, cudaMemcpyHostToDevice, s.s));
+            if (l + 1 < np) {
+                check_view(&d->P[l]);
+                check_view(&d->PT[l]);
+                if (d->P[l].nrows != d->A[l].nrows || d->P[l].ncols != d->A[l + 1].nrows ||
+                    d->PT[l].nrows != d->P[l].ncols || d->PT[l].ncols != d->P[l].nrows)
+                    throw ArgError("hierarchy: transfer dimensions", PMG_ERR_DIM);
+                L.P = make_csr(d->P[l], s.s);
+                L.PT = make_csr(d->PT[l], s.s);
+            }
+        }
+        double ilut_s = 0;
+        for (int l = 0; l + 1 < np; ++l) {
+            if (H->smoother == PMG_SMOOTHER_ILUT) {
+                int rc = make_factor(H->pl[l].A, d->tau, d->fillfactor, d->ordering, &H->pl[l].F, err_row, s.s);
+                if (rc) {
+                    if (err_level) *err_level = l;
+                    return rc;
+                }
+                ilut_s += H->pl[l].F->seconds;
+            } else {
+                ensure_gs(H->pl[l].A, s.s);
+                if (H->pl[l].A->gs_zero_row >= 0) {
+                    if (err_level) *err_level = l;
+                    if (err_row) *err_row = H->pl[l].A->gs_zero_row;
+                    return int(PMG_ZERO_DIAG);
+                }
+            }
+        }
+        H->hl.resize(nh);
+        for (int j = 0; j < nh; ++j) {
+            HLev& L = H->hl[j];
+            if (j == 0) {
+                L.A = H->pl.back().A;
+            } else {
+                check_view(&d->HA[j]);
+                L.A = make_csr(d->HA[j], s.s);
+                L.own_A = true;
+            }
+            if (j + 1 < nh) {
+                check_view(&d->HP[j]);
+                check_view(&d->HPT[j]);
+                L.P = make_csr(d->HP[j], s.s);
+                L.PT = make_csr(d->HPT[j], s.s);
+                int rc = make_factor(L.A, d->tau, d->fillfactor, d->ordering, &L.F, err_row, s.s);
+                if (rc) {
+                    if (err_level) *err_level = np - 1 + j;
+                    return rc;
+                }
+                ilut_s += L.F->seconds;
+            } else {
+                int k = dense_setup(H->coarse, L.A->A, s.s);
+                if (k >= 0) {
+                    if (err_level) *err_level = np - 1 + j;
+                    if (err_row) *err_row = k;
+                    return int(PMG_ZERO_PIVOT);
+                }
+            }
+        }
+        PMG_CUDA(cudaStreamSynchronize(s.s));
+        size_t fr = 0, tot = 0;
+        PMG_CUDA(cudaMemGetInfo(&fr, &tot));
+        H->stats.device_bytes = int64_t(tot - fr);
+        H->stats.ilut_seconds = ilut_s;
+        H->stats.setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        *out = H.release();
+        return int(PMG_OK);
+    });
+}
+
+int pmg_hier_destroy(pmg_hier H) {
+    delete H;
+    return PMG_OK;
+}
+
+int pmg_hier_get_stats(pmg_hier H, pmg_hier_stats* s) {
+    *s = H->stats;
+    return PMG_OK;
+}
+
+int pmg_hier_factor(pmg_hier H, int which, pmg_factor* out) {
+    const int np = int(H->pl.size());
+    if (which < np - 1) {
+        *out = H->pl[which].F;
+    } else {
+        int j = which - (np - 1);
+        if (j < 0 || j >= int(H->hl.size()) - 1) return PMG_ERR_ARG;
+        *out = H->hl[j].F;
+    }
+    return *out ? PMG_OK : PMG_ERR_ARG;
+}
+
+int pmg_work_create(pmg_hier H, pmg_work* out) {
+    return guarded([&] {
+        auto W = std::make_unique<pmg_work_s>();
+        W->H = H;
+        PMG_CUDA(cudaStreamCreateWithFlags(&W->st, cudaStreamNonBlocking));
+        W->pw.resize(H->pl.size());
+        for (size_t l = 0; l < H->pl.size(); ++l) {
+            const size_t n = H->pl[l].A->A.n;
+            PWork& w = W->pw[l];
+            w.u[0] = dalloc<double>(n);
+            w.u[1] = dalloc<double>(n);
+            w.f = dalloc<double>(n);
+            w.r = dalloc<double>(n);
+            w.y = dalloc<double>(n);
+            w.x = dalloc<double>(n);
+        }
+        W->hw.resize(H->hl.size());
+        for (size_t j = 0; j < H->hl.size(); ++j) {
+            const size_t n = H->hl[j].A->A.n;
+            HWork& w = W->hw[j];
+            w.e = dalloc<double>(n);
+            w.r = dalloc<double>(n);
+            w.res = dalloc<double>(n);
+            w.y = dalloc<double>(n);
+            w.x = dalloc<double>(n);
+        }
+        W->ticket = reinterpret_cast<int*>(dalloc<double>(1));
+        const int32_t n0 = H->pl[0].A->A.n;
+        W->nc.partials = dalloc<double>(ceil_div(n0, 256) + 1);
+        W->nc.counter = reinterpret_cast<unsigned*>(dalloc<double>(1));
+        PMG_CUDA(cudaMemset(W->nc.counter, 0, sizeof(double)));
+        W->norm0 = dalloc<double>(1);
+        ensure_hist(*W, 200);
+        *out = W.release();
+        return PMG_OK;
+    });
+}
+
+int pmg_work_destroy(pmg_work W) {
+    delete W;
+    return PMG_OK;
+}
+
+int pmg_solve_device(pmg_work W, const double* d_f, double* d_u, double tol, int max_cycles, double* rho_hist,
+                     int* cycles, int* flags, double* solve_seconds) {
+    return guarded([&] {
+        if (max_cycles < 0) throw ArgError("max_cycles < 0", PMG_ERR_ARG);
+        const int32_t n = W->H->pl[0].A->A.n;
+        PWork& w0 = W->pw[0];
+        w0.cur = 0;
+        PMG_CUDA(cudaMemcpyAsync(w0.u[0], d_u, sizeof(double) * n, cudaMemcpyDeviceToDevice, W->st));
+        int rc = solve_loop(*W, d_f, tol, max_cycles, rho_hist, cycles, flags, solve_seconds);
+        PMG_CUDA(cudaMemcpyAsync(d_u, w0.u[w0.cur], sizeof(double) * n, cudaMemcpyDeviceToDevice, W->st));
+        PMG_CUDA(cudaStreamSynchronize(W->st));
+        return rc;
+    });
+}
+
+int pmg_solve(pmg_work W, const double* f, double* u_inout, double tol, int max_cycles, double* rho_hist, int* cycles,
+              int* flags, double* solve_seconds) {
+    return guarded([&] {
+        if (max_cycles < 0) throw ArgError("max_cycles < 0", PMG_ERR_ARG);
+        const int32_t n = W->H->pl[0].A->A.n;
+        PWork& w0 = W->pw[0];
+        w0.cur = 0;
+        PMG_CUDA(cudaMemcpyAsync(w0.f, f, sizeof(double) * n, cudaMemcpyHostToDevice, W->st));
+        PMG_CUDA(cudaMemcpyAsync(w0.u[0], u_inout, sizeof(double) * n, cudaMemcpyHostToDevice, W->st));
+        int rc = solve_loop(*W, w0.f, tol, max_cycles, rho_hist, cycles, flags, solve_seconds);
+        PMG_CUDA(cudaMemcpyAsync(u_inout, w0.u[w0.cur], sizeof(double) * n, cudaMemcpyDeviceToHost, W->st));
+        PMG_CUDA(cudaStreamSynchronize(W->st));
+        return rc;
+    });
+}
+
+int pmg_cycle(pmg_work W, int level, double* u, const double* f) {
+    return guarded([&] {
+        pmg_hier_s& H = *W->H;
+        if (level < 0 || level >= int(H.pl.size())) throw ArgError("cycle: bad level", PMG_ERR_ARG);
+        const int32_t n = H.pl[level].A->A.n;
+        PWork& w = W->pw[level];
+        w.cur = 0;
+        // f must live in a buffer the cycle does not overwrite: use the level's y buffer
+        // only as a staging area for the coarse levels; level f buffers are overwritten by
+        // restriction, so stage into a dedicated allocation.
+        HostVecs hv;
+        double* df = hv.make(n);
+        PMG_CUDA(cudaMemcpyAsync(df, f, sizeof(double) * n, cudaMemcpyHostToDevice, W->st));
+        PMG_CUDA(cudaMemcpyAsync(w.u[0], u, sizeof(double) * n, cudaMemcpyHostToDevice, W->st));
+        int rc = vcycle(*W, level, df, nullptr, false);
+        PMG_CUDA(cudaMemcpyAsync(u, w.u[w.cur], sizeof(double) * n, cudaMemcpyDeviceToHost, W->st));
+        PMG_CUDA(cudaStreamSynchronize(W->st));
+        return rc;
+    });
+}
+
+int pmg_prolongate(pmg_hier H, int level, const double* vc, double* vf) {
+    return guarded([&] {
+        if (level < 0 || level + 1 >= int(H->pl.size())) throw ArgError("prolongate: bad level", PMG_ERR_ARG);
+        PLev& L = H->pl[level];
+        Stream s;
+        HostVecs hv;
+        double* dc = hv.make(L.P->A.m);
+        double* df = hv.make(L.P->A.n);
+        PMG_CUDA(cudaMemcpyAsync(dc, vc, sizeof(double) * L.P->A.m, cudaMemcpyHostToDevice, s.s));
+        sell_rowop(L.P->S, kOpRestrict, dc, nullptr, L.ML, df, nullptr, s.s);  // (P v) / ML
+        PMG_CUDA(cudaMemcpyAsync(vf, df, sizeof(double) * L.P->A.n, cudaMemcpyDeviceToHost, s.s));
+        PMG_CUDA(cudaStreamSynchronize(s.s));
+        return PMG_OK;
+    });
+}
+
+int pmg_restrict(pmg_hier H, int level, const double* rf, double* rc) {
+    return guarded([&] {
+        if (level < 0 || level + 1 >= int(H->pl.size())) throw ArgError("restrict: bad level", PMG_ERR_ARG);
+        PLev& L = H->pl[level];
+        PLev& C = H->pl[level + 1];
+        Stream s;
+        HostVecs hv;
+        double* dr = hv.make(L.PT->A.m);
+        double* dc = hv.make(L.PT->A.n);
+        PMG_CUDA(cudaMemcpyAsync(dr, rf, sizeof(double) * L.PT->A.m, cudaMemcpyHostToDevice, s.s));
+        sell_rowop(L.PT->S, kOpRestrict, dr, nullptr, C.ML, dc, nullptr, s.s);
+        PMG_CUDA(cudaMemcpyAsync(rc, dc, sizeof(double) * L.PT->A.n, cudaMemcpyDeviceToHost, s.s));
+        PMG_CUDA(cudaStreamSynchronize(s.s));
+        return PMG_OK;
+    });
+}
+
+// ms_by_class[0..6]: resid(A_p), L-solve(p), U-solve(p), GS(p), p-transfers, coarse (p<finest and
+// h-MG), misc; [7] = total launches, [8..14] = launches per class.  enable: n_classes < 0 turns
+// profiling on (-1) / off (-2) and resets the counters.
+int pmg_work_kernel_times(pmg_work W, double* ms, int n) {
+    return guarded([&] {
+        if (n < 0) {
+            W->collect();
+            W->prof = (n == -1);
+            for (int c = 0; c < kNumCls; ++c) {
+                W->cls_ms[c] = 0;
+                W->cls_launches[c] = 0;
+            }
+            W->launches = 0;
+            return PMG_OK;
+        }
+        W->collect();
+        for (int c = 0; c < n && c < kNumCls; ++c) ms[c] = W->cls_ms[c];
+        if (n > kNumCls) ms[kNumCls] = double(W->launches);
+        for (int c = 0; c < kNumCls && kNumCls + 1 + c < n; ++c) ms[kNumCls + 1 + c] = double(W->cls_launches[c]);
+        return PMG_OK;
+    });
+}
+
+}  // extern "C"

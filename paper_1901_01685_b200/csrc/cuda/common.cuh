@@ -1,0 +1,89 @@
+// Shared device helpers for libpmg_cuda (sm_100a, FP64, built with -fmad=false).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+namespace pmg {
+
+struct CudaError : std::runtime_error {
+    int status;
+    CudaError(const std::string& m, int s) : std::runtime_error(m), status(s) {}
+};
+
+#define PMG_CUDA(call)                                                                                        \
+    do {                                                                                                      \
+        cudaError_t e_ = (call);                                                                              \
+        if (e_ != cudaSuccess)                                                                                \
+            throw ::pmg::CudaError(std::string(#call) + ": " + cudaGetErrorString(e_),                        \
+                                   e_ == cudaErrorMemoryAllocation ? 5 /*PMG_ERR_OOM*/ : 4 /*PMG_ERR_CUDA*/); \
+    } while (0)
+
+#define PMG_LAUNCH_CHECK() PMG_CUDA(cudaGetLastError())
+
+constexpr int kSlice = 32;   // SELL slice height = warp width (one row per lane)
+constexpr int kChunk = 256;  // norm / residual block: 8 slices, the canonical norm chunk
+
+// "not yet produced" marker for sync-free solves: a NaN payload no arithmetic produces
+constexpr unsigned long long kSentinelBits = 0xFFF4DEAD0BADF00Dull;
+
+__device__ __forceinline__ double sentinel() { return __longlong_as_double((long long)kSentinelBits); }
+__device__ __forceinline__ bool is_sentinel(double v) {
+    return (unsigned long long)__double_as_longlong(v) == kSentinelBits;
+}
+
+// coherent (L2) load / store of a value produced by another thread during this kernel
+__device__ __forceinline__ double ld_relaxed(const double* p) {
+    double v;
+    asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed(double* p, double v) {
+    asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// spin until another thread has published x[j]
+__device__ __forceinline__ double wait_value(const double* x, int j) {
+    double v = ld_relaxed(x + j);
+    while (is_sentinel(v)) {
+        __nanosleep(20);
+        v = ld_relaxed(x + j);
+    }
+    return v;
+}
+
+// streaming 128-bit loads of matrix data (read once per sweep)
+__device__ __forceinline__ int4 ld_stream_i4(const int4* p) {
+    int4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+__device__ __forceinline__ double2 ld_stream_d2(const double2* p) {
+    double2 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+    return r;
+}
+
+// canonical xor-butterfly over a warp (offsets 16,8,4,2,1); every lane ends with the sum
+__device__ __forceinline__ double warp_butterfly(double v) {
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) v = v + __shfl_xor_sync(0xffffffffu, v, off);
+    return v;
+}
+
+inline int ceil_div(int64_t a, int64_t b) { return int((a + b - 1) / b); }
+
+}  // namespace pmg

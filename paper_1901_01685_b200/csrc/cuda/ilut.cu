@@ -1,0 +1,436 @@
+// GPU ILUT(tau, m) factorisation -- row-parallel IKJ elimination, bit-identical to the
+// oracle.
+//
+// Persistent CTAs claim rows in ascending order through an atomic ticket.  A CTA keeps the
+// working row dense over the band window [i-b, i+b] (b = bandwidth of the permuted matrix;
+// LU fill never leaves the band) in shared memory, with two bitmaps: `pres` (structurally
+// present entries) and `piv` (pending L-part pivots).  Pivots are taken in ascending
+// column order; before using U row k the CTA waits for row k's `done` flag (release /
+// acquire), so the elimination follows the dynamic dependency DAG of the factorisation
+// ("row-parallel elimination over the L-dependency levels").  Row i publishes U first
+// (it gates later rows) and selects its L part afterwards.
+//
+// Per-row arithmetic and dropping are exactly the oracle's:
+//   w_k = w_k / u_kk ; |w_k| < tau_i -> drop ; else w_j = w_j - w_k * u_kj   (ascending k)
+//   U entries |w_j| < tau_i dropped; rule 2 keeps the M largest (|v| desc, col asc) in L and U.
+// Top-M selection is a block-wide MSD radix select on the |v| bit patterns (exact: the
+// kept set under a strict total order is unique, so any exact selection matches).
+#include <cub/device/device_scan.cuh>
+
+#include "ilut.cuh"
+
+namespace pmg {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr unsigned FULL = 0xffffffffu;
+
+struct IlutDev {
+    int32_t n, M, b, W, nwords;
+    const int32_t* rp;
+    const int32_t* ci;
+    const double* v;
+    const double* tau;
+    int32_t* Ucol;
+    double* Uval;
+    int32_t* Ulen;
+    int32_t* Lcol;
+    double* Lval;
+    int32_t* Llen;
+    int* done;
+    int* ticket;
+    int* err_row;
+    double* gw;          // [slots * W] work rows when they do not fit in shared memory
+    int32_t* gcand_col;  // [slots * W]
+    double* gcand_val;
+    int smem_w;
+};
+
+__device__ __forceinline__ uint64_t absbits(double x) {
+    return (unsigned long long)__double_as_longlong(x) & 0x7FFFFFFFFFFFFFFFull;
+}
+
+__device__ __forceinline__ int block_scan_excl(int v, int* sh, int& total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(FULL, x, o);
+        if (lane >= o) x += y;
+    }
+    __syncthreads();
+    if (lane == 31) sh[wid] = x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int acc = 0;
+        for (int w = 0; w < kThreads / 32; ++w) {
+            int t = sh[w];
+            sh[w] = acc;
+            acc += t;
+        }
+        sh[kThreads / 32] = acc;
+    }
+    __syncthreads();
+    total = sh[kThreads / 32];
+    return sh[wid] + x - v;
+}
+
+// gather the band entries [lo, hi) that are present (and, if filter, |w| >= tau) into the
+// candidate arrays in ascending order; returns the count
+__device__ int gather(const double* w, const uint32_t* pres, int lo, int hi, bool filter, double tau, int col0,
+                      int32_t* ccol, double* cval, int* sh) {
+    int base = 0;
+    const int w0 = lo >> 5, w1 = (hi + 31) >> 5;
+    for (int wb = w0; wb < w1; wb += kThreads) {
+        const int wi = wb + threadIdx.x;
+        uint32_t bits = 0;
+        if (wi < w1) {
+            bits = pres[wi];
+            if (wi == (lo >> 5)) bits &= FULL << (lo & 31);
+            if (wi == ((hi - 1) >> 5) && (hi & 31)) bits &= FULL >> (32 - (hi & 31));
+            if (filter) {
+                uint32_t m = bits, keep = 0;
+                while (m) {
+                    int q = __ffs(m) - 1;
+                    m &= m - 1;
+                    if (!(fabs(w[wi * 32 + q]) < tau)) keep |= 1u << q;
+                }
+                bits = keep;
+            }
+        }
+        int tot;
+        int o = block_scan_excl(__popc(bits), sh, tot) + base;
+        while (bits) {
+            int q = __ffs(bits) - 1;
+            bits &= bits - 1;
+            ccol[o] = col0 + wi * 32 + q;
+            cval[o] = w[wi * 32 + q];
+            ++o;
+        }
+        base += tot;
+    }
+    __syncthreads();
+    return base;
+}
+
+// rule 2: keep the M largest |v| (ties by ascending column = candidate order); write the
+// kept entries in ascending column order to (ocol, oval); returns the kept count
+__device__ int select_write(const int32_t* ccol, const double* cval, int C, int M, int32_t* ocol, double* oval,
+                            int* sh, int* hist, uint64_t* s64) {
+    const bool keep_all = C <= M;
+    uint64_t T = 0;
+    int need = 0;
+    if (!keep_all) {
+        if (threadIdx.x == 0) {
+            s64[0] = 0;  // prefix
+            s64[1] = 0;  // mask
+            s64[2] = uint64_t(M);
+        }
+        __syncthreads();
+        for (int shift = 56; shift >= 0; shift -= 8) {
+            hist[threadIdx.x] = 0;  // kThreads == 256 bins
+            __syncthreads();
+            const uint64_t pre = s64[0], msk = s64[1];
+            for (int t = threadIdx.x; t < C; t += kThreads) {
+                uint64_t k = absbits(cval[t]);
+                if ((k & msk) == pre) atomicAdd(&hist[(k >> shift) & 255], 1);
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                int64_t nd = int64_t(s64[2]), cum = 0;
+                int d = 0;
+                for (d = 255; d >= 0; --d) {
+                    if (cum + hist[d] >= nd) break;
+                    cum += hist[d];
+                }
+                s64[0] = pre | (uint64_t(d) << shift);
+                s64[1] = msk | (uint64_t(255) << shift);
+                s64[2] = uint64_t(nd - cum);
+            }
+            __syncthreads();
+        }
+        T = s64[0];
+        need = int(s64[2]);
+    }
+    int base = 0, eqbase = 0;
+    for (int c0 = 0; c0 < C; c0 += kThreads) {
+        const int t = c0 + threadIdx.x;
+        const bool in = t < C;
+        const uint64_t k = in ? absbits(cval[t]) : 0;
+        const bool eq = in && !keep_all && k == T;
+        int eqtot, ktot;
+        const int eqr = block_scan_excl(eq ? 1 : 0, sh, eqtot) + eqbase;
+        const bool keep = in && (keep_all || k > T || (eq && eqr < need));
+        const int kr = block_scan_excl(keep ? 1 : 0, sh, ktot);
+        if (keep) {
+            ocol[base + kr] = ccol[t];
+            oval[base + kr] = cval[t];
+        }
+        base += ktot;
+        eqbase += eqtot;
+    }
+    __syncthreads();
+    return base;
+}
+
+__global__ void __launch_bounds__(kThreads) k_ilut(IlutDev d) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ int sh[kThreads / 32 + 1];
+    __shared__ int hist[256];
+    __shared__ uint64_t s64[3];
+    __shared__ int s_row, s_k, s_go, s_ulen;
+    __shared__ double s_wk;
+    uint32_t* pres = reinterpret_cast<uint32_t*>(smem);
+    uint32_t* piv = pres + d.nwords;
+    double* w = d.smem_w ? reinterpret_cast<double*>(smem + ((size_t(2 * d.nwords) * 4 + 15) & ~size_t(15)))
+                         : d.gw + size_t(blockIdx.x) * d.W;
+    int32_t* ccol = d.gcand_col + size_t(blockIdx.x) * d.W;
+    double* cval = d.gcand_val + size_t(blockIdx.x) * d.W;
+    const int b = d.b, M = d.M;
+
+    for (int q = threadIdx.x; q < d.W; q += kThreads) w[q] = 0.0;
+    for (int q = threadIdx.x; q < 2 * d.nwords; q += kThreads) pres[q] = 0;
+    __syncthreads();
+
+    for (;;) {
+        if (threadIdx.x == 0) s_row = atomicAdd(d.ticket, 1);
+        __syncthreads();
+        const int i = s_row;
+        if (i >= d.n) break;
+        // scatter row i of the permuted matrix into the band window
+        for (int q = d.rp[i] + threadIdx.x; q < d.rp[i + 1]; q += kThreads) {
+            const int jb = d.ci[q] - i + b;
+            w[jb] = d.v[q];
+            atomicOr(&pres[jb >> 5], 1u << (jb & 31));
+            if (jb < b) atomicOr(&piv[jb >> 5], 1u << (jb & 31));
+        }
+        const double tau_i = d.tau[i];
+        __syncthreads();
+        int kb = 0;
+        const int nwl = (b + 31) >> 5;
+        for (;;) {
+            if (threadIdx.x < 32) {  // next pending pivot >= kb
+                int found = -1;
+                for (int wb = kb >> 5; wb < nwl && found < 0; wb += 32) {
+                    const int wi = wb + threadIdx.x;
+                    uint32_t bits = wi < nwl ? piv[wi] : 0u;
+                    if (wi == (kb >> 5)) bits &= FULL << (kb & 31);
+                    const uint32_t bal = __ballot_sync(FULL, bits != 0u);
+                    if (bal) {
+                        const int fl = __ffs(bal) - 1;
+                        const uint32_t wbits = __shfl_sync(FULL, bits, fl);
+                        found = (wb + fl) * 32 + __ffs(wbits) - 1;
+                    }
+                }
+                if (threadIdx.x == 0) s_k = found;
+            }
+            __syncthreads();
+            const int k = s_k;
+            if (k < 0) break;
+            if (threadIdx.x == 0) {
+                piv[k >> 5] &= ~(1u << (k & 31));
+                const int jk = i - b + k;
+                while (ld_acquire(d.done + jk) == 0) __nanosleep(40);
+                const size_t ub = size_t(jk) * (M + 1);
+                const double wk = w[k] / __ldcg(d.Uval + ub);
+                if (fabs(wk) < tau_i) {
+                    w[k] = 0.0;
+                    pres[k >> 5] &= ~(1u << (k & 31));
+                    s_go = 0;
+                } else {
+                    w[k] = wk;
+                    s_wk = wk;
+                    s_go = 1;
+                    s_ulen = __ldcg(d.Ulen + jk);
+                }
+            }
+            __syncthreads();
+            if (s_go) {
+                const int jk = i - b + k;
+                const size_t ub = size_t(jk) * (M + 1) + 1;
+                const double wk = s_wk;
+                for (int q = threadIdx.x; q < s_ulen - 1; q += kThreads) {
+                    const int jb = __ldcg(d.Ucol + ub + q) - i + b;
+                    const double uv = __ldcg(d.Uval + ub + q);
+                    const uint32_t bit = 1u << (jb & 31);
+                    const uint32_t old = atomicOr(&pres[jb >> 5], bit);
+                    if (!(old & bit) && jb < b) atomicOr(&piv[jb >> 5], bit);
+                    w[jb] = w[jb] - wk * uv;
+                }
+            }
+            __syncthreads();
+            kb = k + 1;
+        }
+        // ---- U part: diagonal + selected off-diagonals, published first
+        double diag = w[b];
+        const bool has_diag = (pres[b >> 5] >> (b & 31)) & 1u;
+        if (!has_diag || diag == 0.0) {
+            if (threadIdx.x == 0) atomicMin(d.err_row, i);
+            diag = 1.0;  // keep going so that no other CTA deadlocks; the host reports err_row
+        }
+        int C = gather(w, pres, b + 1, d.W, true, tau_i, i - b, ccol, cval, sh);
+        const size_t ub = size_t(i) * (M + 1);
+        int nu = select_write(ccol, cval, C, M, d.Ucol + ub + 1, d.Uval + ub + 1, sh, hist, s64);
+        __threadfence();  // every writer orders its U entries before the release below
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            d.Ucol[ub] = i;
+            d.Uval[ub] = diag;
+            d.Ulen[i] = nu + 1;
+            __threadfence();
+            st_release(d.done + i, 1);
+        }
+        // ---- L part: the kept multipliers
+        C = gather(w, pres, 0, b, false, 0.0, i - b, ccol, cval, sh);
+        const size_t lb = size_t(i) * M;
+        int nl = select_write(ccol, cval, C, M, d.Lcol + lb, d.Lval + lb, sh, hist, s64);
+        if (threadIdx.x == 0) d.Llen[i] = nl;
+        // ---- reset the window
+        for (int wi = threadIdx.x; wi < d.nwords; wi += kThreads) {
+            uint32_t bits = pres[wi];
+            while (bits) {
+                int q = __ffs(bits) - 1;
+                bits &= bits - 1;
+                w[wi * 32 + q] = 0.0;
+            }
+            pres[wi] = 0;
+        }
+        __syncthreads();
+    }
+}
+
+// tau_i = tau * (sum_j |a_ij| / nnz_i), ascending column (oracle order)
+__global__ void k_row_tau(int32_t n, const int32_t* __restrict__ rp, const double* __restrict__ v, double tau,
+                          double* __restrict__ out) {
+    int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double s = 0.0;
+    for (int32_t k = rp[i]; k < rp[i + 1]; ++k) s = s + fabs(v[k]);
+    out[i] = tau * (s / double(rp[i + 1] - rp[i]));
+}
+
+__global__ void k_compact(int32_t n, int stride, const int32_t* __restrict__ len, const int32_t* __restrict__ pcol,
+                          const double* __restrict__ pval, const int32_t* __restrict__ rowptr, int32_t* __restrict__ col,
+                          double* __restrict__ val) {
+    int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const size_t src = size_t(i) * stride;
+    const int32_t dst = rowptr[i];
+    for (int q = 0; q < len[i]; ++q) {
+        col[dst + q] = pcol[src + q];
+        val[dst + q] = pval[src + q];
+    }
+}
+
+void compact_rows(int32_t n, int stride, const int32_t* len, const int32_t* pcol, const double* pval, DevCsr& out,
+                  cudaStream_t st) {
+    out.n = out.m = n;
+    PMG_CUDA(cudaMallocAsync(&out.rowptr, sizeof(int32_t) * (n + 1), st));
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, len, out.rowptr, n + 1, st);
+    void* tmp;
+    PMG_CUDA(cudaMallocAsync(&tmp, tb, st));
+    // len has n entries; scan n+1 with a zero tail: copy into a padded buffer first
+    int32_t* lp;
+    PMG_CUDA(cudaMallocAsync(&lp, sizeof(int32_t) * (n + 1), st));
+    PMG_CUDA(cudaMemcpyAsync(lp, len, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, st));
+    PMG_CUDA(cudaMemsetAsync(lp + n, 0, sizeof(int32_t), st));
+    cub::DeviceScan::ExclusiveSum(tmp, tb, lp, out.rowptr, n + 1, st);
+    int32_t nnz = 0;
+    PMG_CUDA(cudaMemcpyAsync(&nnz, out.rowptr + n, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    PMG_CUDA(cudaStreamSynchronize(st));
+    out.nnz = nnz;
+    PMG_CUDA(cudaMallocAsync(&out.col, sizeof(int32_t) * std::max(nnz, 1), st));
+    PMG_CUDA(cudaMallocAsync(&out.val, sizeof(double) * std::max(nnz, 1), st));
+    k_compact<<<ceil_div(n, 256), 256, 0, st>>>(n, stride, len, pcol, pval, out.rowptr, out.col, out.val);
+    PMG_LAUNCH_CHECK();
+    PMG_CUDA(cudaFreeAsync(tmp, st));
+    PMG_CUDA(cudaFreeAsync(lp, st));
+}
+
+}  // namespace
+
+int ilut_factorize_device(const DevCsr& A, int32_t band, double tau, double fillfactor, DevCsr& L, DevCsr& U,
+                          int64_t* err_row, double* seconds, cudaStream_t st) {
+    const int32_t n = A.n;
+    const int32_t M = int32_t(std::ceil(fillfactor * double(A.nnz) / double(n)));
+    const int32_t b = std::max(band, 1);
+    const int32_t W = 2 * b + 1;
+    const int32_t nwords = (W + 31) / 32;
+    cudaEvent_t e0, e1;
+    PMG_CUDA(cudaEventCreate(&e0));
+    PMG_CUDA(cudaEventCreate(&e1));
+    PMG_CUDA(cudaEventRecord(e0, st));
+
+    int dev = 0, nsm = 0;
+    PMG_CUDA(cudaGetDevice(&dev));
+    PMG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    int max_smem = 0;
+    PMG_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    const size_t bits_bytes = (size_t(2 * nwords) * 4 + 15) & ~size_t(15);
+    const size_t static_bytes = 4096;
+    size_t dyn = bits_bytes + size_t(W) * 8;
+    int smem_w = 1;
+    if (dyn + static_bytes > size_t(max_smem)) {
+        smem_w = 0;
+        dyn = bits_bytes;
+    }
+    if (dyn + static_bytes > size_t(max_smem)) throw CudaError("ilut: band too wide for the bitmaps", 6);
+    PMG_CUDA(cudaFuncSetAttribute(k_ilut, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dyn)));
+    int occ = 0;
+    PMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_ilut, kThreads, dyn));
+    occ = std::max(1, std::min(occ, 4));
+    const int grid = std::min<int64_t>(int64_t(nsm) * occ, std::max<int32_t>(n, 1));
+
+    IlutDev d{};
+    d.n = n; d.M = M; d.b = b; d.W = W; d.nwords = nwords;
+    d.rp = A.rowptr; d.ci = A.col; d.v = A.val;
+    d.smem_w = smem_w;
+    PMG_CUDA(cudaMallocAsync(&d.tau, sizeof(double) * n, st));
+    k_row_tau<<<ceil_div(n, 256), 256, 0, st>>>(n, A.rowptr, A.val, tau, const_cast<double*>(d.tau));
+    PMG_LAUNCH_CHECK();
+    PMG_CUDA(cudaMallocAsync(&d.Ucol, sizeof(int32_t) * size_t(n) * (M + 1), st));
+    PMG_CUDA(cudaMallocAsync(&d.Uval, sizeof(double) * size_t(n) * (M + 1), st));
+    PMG_CUDA(cudaMallocAsync(&d.Ulen, sizeof(int32_t) * n, st));
+    PMG_CUDA(cudaMallocAsync(&d.Lcol, sizeof(int32_t) * size_t(n) * std::max(M, 1), st));
+    PMG_CUDA(cudaMallocAsync(&d.Lval, sizeof(double) * size_t(n) * std::max(M, 1), st));
+    PMG_CUDA(cudaMallocAsync(&d.Llen, sizeof(int32_t) * n, st));
+    PMG_CUDA(cudaMallocAsync(&d.done, sizeof(int) * n, st));
+    PMG_CUDA(cudaMallocAsync(&d.ticket, sizeof(int) * 2, st));
+    d.err_row = d.ticket + 1;
+    PMG_CUDA(cudaMallocAsync(&d.gcand_col, sizeof(int32_t) * size_t(grid) * W, st));
+    PMG_CUDA(cudaMallocAsync(&d.gcand_val, sizeof(double) * size_t(grid) * W, st));
+    d.gw = nullptr;
+    if (!smem_w) PMG_CUDA(cudaMallocAsync(&d.gw, sizeof(double) * size_t(grid) * W, st));
+    PMG_CUDA(cudaMemsetAsync(d.done, 0, sizeof(int) * n, st));
+    int init[2] = {0, 0x7fffffff};
+    PMG_CUDA(cudaMemcpyAsync(d.ticket, init, sizeof(init), cudaMemcpyHostToDevice, st));
+    k_ilut<<<grid, kThreads, dyn, st>>>(d);
+    PMG_LAUNCH_CHECK();
+    int er = 0;
+    PMG_CUDA(cudaMemcpyAsync(&er, d.err_row, sizeof(int), cudaMemcpyDeviceToHost, st));
+    PMG_CUDA(cudaStreamSynchronize(st));
+    int status = 0;
+    if (er != 0x7fffffff) {
+        if (err_row) *err_row = er;
+        status = 1;  // PMG_ZERO_PIVOT
+    } else {
+        compact_rows(n, M, d.Llen, d.Lcol, d.Lval, L, st);
+        compact_rows(n, M + 1, d.Ulen, d.Ucol, d.Uval, U, st);
+    }
+    PMG_CUDA(cudaEventRecord(e1, st));
+    PMG_CUDA(cudaEventSynchronize(e1));
+    float ms = 0;
+    PMG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    if (seconds) *seconds = ms * 1e-3;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    for (void* p : {(void*)d.tau, (void*)d.Ucol, (void*)d.Uval, (void*)d.Ulen, (void*)d.Lcol, (void*)d.Lval,
+                    (void*)d.Llen, (void*)d.done, (void*)d.ticket, (void*)d.gcand_col, (void*)d.gcand_val, (void*)d.gw})
+        if (p) PMG_CUDA(cudaFreeAsync(p, st));
+    PMG_CUDA(cudaStreamSynchronize(st));
+    return status;
+}
+
+}  // namespace pmg

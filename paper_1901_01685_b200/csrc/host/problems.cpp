@@ -1,0 +1,303 @@
+// Benchmark problems and the p-multigrid level hierarchy inputs (host, setup only).
+//
+//   BASELINE.json configs 1..5 (unit square / quarter annulus / CDR / L-shape / large
+//   annulus) and the paper's Benchmarks 1-2 used to pin the oracle.
+//   Degree lists per SURVEY D7; h-MG chain down to h = 2^-2;
+//   seeded initial guess = splitmix64 -> U[-1,1).
+//
+// Exposed through the C ABI in include/iga_host.h.
+#include <cmath>
+#include <cstring>
+#include <memory>
+
+#include "discretization.hpp"
+#include "../../../include/iga_host.h"
+
+namespace iga {
+
+struct HLevel {
+    HostCsr A, P, PT;  // P: prolongation from the next coarser h-level to this one
+};
+struct PLevel {
+    int degree = 1;
+    HostCsr A;
+    std::vector<double> ML;
+    HostCsr P, PT;  // P: from the next lower degree to this one (empty on the last level)
+};
+struct Problem {
+    std::vector<PLevel> plev;
+    std::vector<HLevel> hlev;  // hlev[0].A is empty: the finest h-level is plev.back()
+    std::vector<double> f, u0;
+    int nel = 0;
+};
+
+static uint64_t splitmix64(uint64_t& s) {
+    uint64_t z = (s += 0x9E3779B97F4A7C15ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+static Domain make_domain(int geometry) {
+    Domain d;
+    if (geometry == IGA_GEOM_SQUARE) d.patches.push_back(NurbsPatch::affine(0, 0, 1, 1));
+    else if (geometry == IGA_GEOM_ANNULUS) d.patches.push_back(NurbsPatch::quarter_annulus(1.0, 2.0));
+    else if (geometry == IGA_GEOM_LSHAPE) {
+        // 3 unit squares (-1,0)x(0,1), (-1,0)x(-1,0), (0,1)x(-1,0)
+        d.patches.push_back(NurbsPatch::affine(-1, 0, 1, 1));
+        d.patches.push_back(NurbsPatch::affine(-1, -1, 1, 1));
+        d.patches.push_back(NurbsPatch::affine(0, -1, 1, 1));
+        d.glue.push_back({1, 2, 0, 0});  // patch1 top  == patch0 bottom
+        d.glue.push_back({2, 3, 1, 1});  // patch2 left == patch1 right
+    } else
+        throw ConfigError("unknown geometry");
+    return d;
+}
+
+static Cdr make_coeffs(int rhs_kind, const double* D, const double* v, double R) {
+    Cdr c;
+    for (int i = 0; i < 4; ++i) c.D[i / 2][i % 2] = D[i];
+    c.v[0] = v[0];
+    c.v[1] = v[1];
+    c.R = R;
+    switch (rhs_kind) {
+        case IGA_RHS_SINSIN:  // config 1: 2 pi^2 sin(pi x) sin(pi y)
+            c.f = [](double x, double y) { return 2.0 * M_PI * M_PI * std::sin(M_PI * x) * std::sin(M_PI * y); };
+            break;
+        case IGA_RHS_ANNULUS:  // configs 2/5: -(8 - 9 r) sin(2 atan(y/x)) / r^2
+            c.f = [](double x, double y) {
+                double r2 = x * x + y * y;
+                return -(8.0 - 9.0 * std::sqrt(r2)) * std::sin(2.0 * std::atan2(y, x)) / r2;
+            };
+            break;
+        case IGA_RHS_ONE:
+            c.f = [](double, double) { return 1.0; };
+            break;
+        case IGA_RHS_B1: {  // paper Benchmark 1: u = -(r^2-1)(r^2-4) x y^2, f = -lap u
+            c.f = [](double x, double y) {
+                double s = x * x + y * y;
+                return 2.0 * x * (s * s - 5.0 * s + 4.0) + x * y * y * (40.0 * s - 80.0);
+            };
+            break;
+        }
+        case IGA_RHS_B2: {  // paper Benchmark 2: u = sin(pi x) sin(pi y), f = -div(D grad u) + v.grad u + R u
+            double D00 = D[0], D01 = D[1], D10 = D[2], D11 = D[3], v0 = v[0], v1 = v[1];
+            c.f = [=](double x, double y) {
+                double sx = std::sin(M_PI * x), sy = std::sin(M_PI * y), cx = std::cos(M_PI * x), cy = std::cos(M_PI * y);
+                double pi2 = M_PI * M_PI;
+                return pi2 * (D00 + D11) * sx * sy - (D01 + D10) * pi2 * cx * cy + v0 * M_PI * cx * sy + v1 * M_PI * sx * cy +
+                       R * sx * sy;
+            };
+            break;
+        }
+        default:
+            throw ConfigError("unknown rhs kind");
+    }
+    return c;
+}
+
+static Problem build_problem(const iga_problem_spec& s) {
+    if (s.n_degrees < 1 || s.n_degrees > 8) throw ConfigError("degree list length");
+    if (s.degrees[s.n_degrees - 1] != 1) throw ConfigError("degree list must end at 1");
+    for (int i = 1; i < s.n_degrees; ++i)
+        if (!(s.degrees[i] < s.degrees[i - 1])) throw ConfigError("degrees must be strictly decreasing");
+    if (s.h_exp < 2 || s.h_exp > 12) throw ConfigError("h_exp out of range");
+    if (s.coarsest_h_exp < 1 || s.coarsest_h_exp > s.h_exp) throw ConfigError("coarsest_h_exp out of range");
+    Domain dom = make_domain(s.geometry);
+    Cdr c = make_coeffs(s.rhs, s.D, s.v, s.R);
+    c.nitsche_scale = s.nitsche_scale > 0 ? s.nitsche_scale : 1.0;
+    Cdr c_nof = c;
+    c_nof.f = nullptr;
+    const int nel = 1 << s.h_exp;
+    Problem pb;
+    pb.nel = nel;
+    std::vector<Space> spaces;
+    for (int l = 0; l < s.n_degrees; ++l) spaces.push_back(Space::build(dom, s.degrees[l], nel));
+    pb.plev.resize(s.n_degrees);
+    for (int l = 0; l < s.n_degrees; ++l) {
+        PLevel& L = pb.plev[l];
+        L.degree = s.degrees[l];
+        L.A = assemble_operator(dom, spaces[l], l == 0 ? c : c_nof, l == 0 ? &pb.f : nullptr);
+        L.ML = lumped_mass(dom, spaces[l]);
+        if (l + 1 < s.n_degrees) {
+            L.P = assemble_transfer(dom, spaces[l], spaces[l + 1]);
+            L.PT = transpose(L.P);
+        }
+    }
+    // h-levels at p = 1: h, 2h, ... down to 2^-coarsest (rediscretised)
+    pb.hlev.resize(s.h_exp - s.coarsest_h_exp + 1);
+    Space fine = spaces.back();
+    for (size_t j = 1; j < pb.hlev.size(); ++j) {
+        Space coarse = Space::build(dom, 1, nel >> j);
+        pb.hlev[j].A = assemble_operator(dom, coarse, c_nof, nullptr);
+        pb.hlev[j - 1].P = hrefine_p1(dom, fine, coarse);
+        pb.hlev[j - 1].PT = transpose(pb.hlev[j - 1].P);
+        fine = coarse;
+    }
+    const int32_t N = spaces[0].ndof;
+    pb.u0.assign(N, 0.0);
+    if (s.random_guess) {
+        uint64_t st = s.seed;
+        for (int32_t i = 0; i < N; ++i) pb.u0[i] = double(splitmix64(st) >> 11) * 0x1.0p-53 * 2.0 - 1.0;
+    }
+    return pb;
+}
+
+}  // namespace iga
+
+// =================================================================== C ABI
+using namespace iga;
+
+struct iga_problem_s {
+    Problem pb;
+};
+
+static thread_local std::string g_err;
+
+extern "C" {
+
+const char* iga_last_error(void) { return g_err.c_str(); }
+
+void iga_set_num_threads(int n) { set_num_threads(n); }
+
+int iga_config_spec(int config, int degree, iga_problem_spec* s) {
+    std::memset(s, 0, sizeof(*s));
+    s->D[0] = s->D[3] = 1.0;
+    s->coarsest_h_exp = 2;
+    s->seed = 0;
+    switch (config) {
+        case 1:
+            s->geometry = IGA_GEOM_SQUARE; s->rhs = IGA_RHS_SINSIN; s->h_exp = 5;
+            s->n_degrees = 2; s->degrees[0] = 2; s->degrees[1] = 1;
+            break;
+        case 2:
+            if (degree < 2 || degree > 4) degree = 2;
+            s->geometry = IGA_GEOM_ANNULUS; s->rhs = IGA_RHS_ANNULUS; s->h_exp = 7;
+            s->n_degrees = 2; s->degrees[0] = degree; s->degrees[1] = 1;
+            break;
+        case 3:
+            s->geometry = IGA_GEOM_SQUARE; s->rhs = IGA_RHS_ONE; s->h_exp = 8;
+            s->v[0] = 2; s->v[1] = 3; s->R = 3;
+            s->n_degrees = 3; s->degrees[0] = 3; s->degrees[1] = 2; s->degrees[2] = 1;
+            s->random_guess = 1; s->seed = 0;
+            break;
+        case 4:
+            s->geometry = IGA_GEOM_LSHAPE; s->rhs = IGA_RHS_ONE; s->h_exp = 8;
+            s->n_degrees = 2; s->degrees[0] = 4; s->degrees[1] = 1;
+            break;
+        case 5:
+            s->geometry = IGA_GEOM_ANNULUS; s->rhs = IGA_RHS_ANNULUS; s->h_exp = 10;
+            s->n_degrees = 2; s->degrees[0] = 5; s->degrees[1] = 1;
+            break;
+        default:
+            g_err = "unknown config";
+            return -1;
+    }
+    return 0;
+}
+
+int iga_problem_build(const iga_problem_spec* s, iga_problem** out) {
+    try {
+        auto* h = new iga_problem_s;
+        h->pb = build_problem(*s);
+        *out = h;
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        *out = nullptr;
+        return -1;
+    }
+}
+
+void iga_problem_free(iga_problem* h) { delete h; }
+
+int iga_problem_num_plevels(const iga_problem* h) { return int(h->pb.plev.size()); }
+int iga_problem_num_hlevels(const iga_problem* h) { return int(h->pb.hlev.size()); }
+int iga_problem_degree(const iga_problem* h, int l) { return h->pb.plev.at(l).degree; }
+
+static const HostCsr* pick(const iga_problem* h, int kind, int l) {
+    const Problem& pb = h->pb;
+    switch (kind) {
+        case IGA_MAT_A: return &pb.plev.at(l).A;
+        case IGA_MAT_P: return &pb.plev.at(l).P;
+        case IGA_MAT_PT: return &pb.plev.at(l).PT;
+        case IGA_MAT_HA: return l == 0 ? &pb.plev.back().A : &pb.hlev.at(l).A;
+        case IGA_MAT_HP: return &pb.hlev.at(l).P;
+        case IGA_MAT_HPT: return &pb.hlev.at(l).PT;
+    }
+    return nullptr;
+}
+
+int iga_problem_csr_shape(const iga_problem* h, int kind, int l, int32_t* nrows, int32_t* ncols, int64_t* nnz) {
+    try {
+        const HostCsr* A = pick(h, kind, l);
+        if (!A) return -1;
+        *nrows = A->nrows;
+        *ncols = A->ncols;
+        *nnz = A->nnz();
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
+int iga_problem_csr_copy(const iga_problem* h, int kind, int l, int32_t* rowptr, int32_t* col, double* val) {
+    try {
+        const HostCsr* A = pick(h, kind, l);
+        if (!A) return -1;
+        if (A->nnz() > INT32_MAX) { g_err = "nnz exceeds int32"; return -1; }
+        for (int32_t i = 0; i <= A->nrows; ++i) rowptr[i] = int32_t(A->rowptr[i]);
+        std::memcpy(col, A->col.data(), A->col.size() * sizeof(int32_t));
+        std::memcpy(val, A->val.data(), A->val.size() * sizeof(double));
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
+int iga_problem_vec_len(const iga_problem* h, int kind, int l) {
+    const Problem& pb = h->pb;
+    if (kind == IGA_VEC_ML) return int(pb.plev.at(l).ML.size());
+    if (kind == IGA_VEC_F) return int(pb.f.size());
+    if (kind == IGA_VEC_U0) return int(pb.u0.size());
+    return -1;
+}
+
+int iga_problem_vec_copy(const iga_problem* h, int kind, int l, double* out) {
+    const Problem& pb = h->pb;
+    const std::vector<double>* v = nullptr;
+    if (kind == IGA_VEC_ML) v = &pb.plev.at(l).ML;
+    if (kind == IGA_VEC_F) v = &pb.f;
+    if (kind == IGA_VEC_U0) v = &pb.u0;
+    if (!v) return -1;
+    std::memcpy(out, v->data(), v->size() * sizeof(double));
+    return 0;
+}
+
+// ---- small entry points mirroring SPEC ops, used by the property tests ----
+int iga_eval_basis(int p, int spans, double x, int with_deriv, double* N, double* dN) {
+    try {
+        Knots kv = Knots::open_uniform(p, spans);
+        return with_deriv ? basis_values_d1(kv, x, N, dN) : basis_values(kv, x, N);
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
+int iga_geometry_map(int geometry, int patch, double xi, double eta, double* X, double* J) {
+    try {
+        Domain d = make_domain(geometry);
+        double Jm[2][2];
+        d.patches.at(patch).map(xi, eta, X, Jm);
+        J[0] = Jm[0][0]; J[1] = Jm[0][1]; J[2] = Jm[1][0]; J[3] = Jm[1][1];
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
+}  // extern "C"

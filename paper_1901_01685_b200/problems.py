@@ -1,0 +1,198 @@
+"""Problem / hierarchy inputs (host assembly through ``libiga_host.so``).
+
+The BASELINE.json configs 1-5 and the paper's Benchmarks 1-2.
+Assembly is setup, not the solve path; it produces the FP64 CSR
+operators both the CUDA path and the CPU oracle consume.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from ._native import Csr, load, ptr
+
+GEOM = {"square": 0, "annulus": 1, "lshape": 2}
+RHS = {"sinsin": 0, "annulus": 1, "one": 2, "b1": 3, "b2": 4}
+MAT_A, MAT_P, MAT_PT, MAT_HA, MAT_HP, MAT_HPT = range(6)
+VEC_ML, VEC_F, VEC_U0 = range(3)
+
+
+class ProblemSpec(ctypes.Structure):
+    _fields_ = [
+        ("geometry", ctypes.c_int), ("rhs", ctypes.c_int), ("D", ctypes.c_double * 4),
+        ("v", ctypes.c_double * 2), ("R", ctypes.c_double), ("h_exp", ctypes.c_int),
+        ("coarsest_h_exp", ctypes.c_int), ("n_degrees", ctypes.c_int), ("degrees", ctypes.c_int * 8),
+        ("random_guess", ctypes.c_int), ("seed", ctypes.c_uint64), ("nitsche_scale", ctypes.c_double),
+    ]
+
+
+def _host():
+    lib = load("libiga_host.so")
+    if not getattr(lib, "_typed", False):
+        lib.iga_last_error.restype = ctypes.c_char_p
+        lib.iga_problem_build.argtypes = [ctypes.POINTER(ProblemSpec), ctypes.POINTER(ctypes.c_void_p)]
+        lib.iga_problem_free.argtypes = [ctypes.c_void_p]
+        for fn in ("iga_problem_num_plevels", "iga_problem_num_hlevels"):
+            getattr(lib, fn).argtypes = [ctypes.c_void_p]
+        lib.iga_problem_degree.argtypes = [ctypes.c_void_p, ctypes.c_int]
+        lib.iga_problem_csr_shape.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                              ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
+                                              ctypes.POINTER(ctypes.c_int64)]
+        lib.iga_problem_csr_copy.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                             ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+        lib.iga_problem_vec_len.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
+        lib.iga_problem_vec_copy.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
+        lib.iga_config_spec.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ProblemSpec)]
+        lib.iga_eval_basis.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_int,
+                                       ctypes.c_void_p, ctypes.c_void_p]
+        lib.iga_geometry_map.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_double,
+                                         ctypes.c_void_p, ctypes.c_void_p]
+        lib.iga_set_num_threads.argtypes = [ctypes.c_int]
+        lib._typed = True
+    return lib
+
+
+def _check(rc):
+    if rc != 0:
+        raise RuntimeError(_host().iga_last_error().decode())
+
+
+@dataclass
+class PLevel:
+    degree: int
+    A: Csr
+    ML: np.ndarray
+    P: Csr | None = None   # prolongation from the next (lower-degree) level to this one
+    PT: Csr | None = None
+
+
+@dataclass
+class HLevel:
+    A: Csr
+    P: Csr | None = None   # prolongation from the next coarser h-level
+    PT: Csr | None = None
+
+
+@dataclass
+class Problem:
+    name: str
+    spec: dict
+    plevels: list[PLevel]
+    hlevels: list[HLevel]   # hlevels[0].A is plevels[-1].A
+    f: np.ndarray
+    u0: np.ndarray
+    extra: dict = field(default_factory=dict)
+
+    @property
+    def n(self) -> int:
+        return self.plevels[0].A.nrows
+
+
+def config_spec(config: int, degree: int = 0) -> ProblemSpec:
+    s = ProblemSpec()
+    _check(_host().iga_config_spec(config, degree, ctypes.byref(s)))
+    return s
+
+
+def make_spec(geometry="square", rhs="one", degrees=(2, 1), h_exp=4, D=(1, 0, 0, 1), v=(0, 0), R=0.0,
+              random_guess=False, seed=42, coarsest_h_exp=2) -> ProblemSpec:
+    s = ProblemSpec()
+    s.geometry = GEOM[geometry]
+    s.rhs = RHS[rhs]
+    for i, d in enumerate(D):
+        s.D[i] = d
+    s.v[0], s.v[1] = v
+    s.R = R
+    s.h_exp = h_exp
+    s.coarsest_h_exp = coarsest_h_exp
+    s.n_degrees = len(degrees)
+    for i, d in enumerate(degrees):
+        s.degrees[i] = d
+    s.random_guess = int(bool(random_guess))
+    s.seed = seed
+    return s
+
+
+def benchmark_spec(bench: int, p: int, h_exp: int, consecutive=True, seed=42) -> ProblemSpec:
+    """Paper Benchmarks 1/2 with the paper's random initial guess."""
+    degrees = tuple(range(p, 0, -1)) if consecutive else (p, 1)
+    if bench == 1:
+        return make_spec("annulus", "b1", degrees, h_exp, random_guess=True, seed=seed)
+    if bench == 2:
+        return make_spec("square", "b2", degrees, h_exp, D=(1.2, -0.7, -0.4, 0.9), v=(0.4, -0.2), R=0.3,
+                         random_guess=True, seed=seed)
+    raise ValueError(bench)
+
+
+def set_threads(n: int) -> None:
+    _host().iga_set_num_threads(n)
+
+
+def _csr(lib, h, kind, l) -> Csr:
+    nr, nc, nnz = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int64()
+    _check(lib.iga_problem_csr_shape(h, kind, l, ctypes.byref(nr), ctypes.byref(nc), ctypes.byref(nnz)))
+    rowptr = np.empty(nr.value + 1, np.int32)
+    col = np.empty(nnz.value, np.int32)
+    val = np.empty(nnz.value, np.float64)
+    _check(lib.iga_problem_csr_copy(h, kind, l, ptr(rowptr), ptr(col), ptr(val)))
+    return Csr(nr.value, nc.value, rowptr, col, val)
+
+
+def _vec(lib, h, kind, l) -> np.ndarray:
+    n = lib.iga_problem_vec_len(h, kind, l)
+    out = np.empty(n, np.float64)
+    _check(lib.iga_problem_vec_copy(h, kind, l, ptr(out)))
+    return out
+
+
+def build(spec: ProblemSpec | int, degree: int = 0, name: str | None = None) -> Problem:
+    """Assemble a problem: ``spec`` is a ProblemSpec or a BASELINE config number 1..5."""
+    if isinstance(spec, int):
+        name = name or (f"config{spec}" + (f"_p{degree}" if spec == 2 else ""))
+        spec = config_spec(spec, degree)
+    lib = _host()
+    h = ctypes.c_void_p()
+    _check(lib.iga_problem_build(ctypes.byref(spec), ctypes.byref(h)))
+    try:
+        npl = lib.iga_problem_num_plevels(h)
+        nhl = lib.iga_problem_num_hlevels(h)
+        pl = []
+        for l in range(npl):
+            lev = PLevel(lib.iga_problem_degree(h, l), _csr(lib, h, MAT_A, l), _vec(lib, h, VEC_ML, l))
+            if l + 1 < npl:
+                lev.P = _csr(lib, h, MAT_P, l)
+                lev.PT = _csr(lib, h, MAT_PT, l)
+            pl.append(lev)
+        hl = []
+        for j in range(nhl):
+            A = pl[-1].A if j == 0 else _csr(lib, h, MAT_HA, j)
+            lev = HLevel(A)
+            if j + 1 < nhl:
+                lev.P = _csr(lib, h, MAT_HP, j)
+                lev.PT = _csr(lib, h, MAT_HPT, j)
+            hl.append(lev)
+        f = _vec(lib, h, VEC_F, 0)
+        u0 = _vec(lib, h, VEC_U0, 0)
+    finally:
+        lib.iga_problem_free(h)
+    sd = {k: (list(getattr(spec, k)) if k in ("D", "v", "degrees") else getattr(spec, k)) for k, _ in spec._fields_}
+    sd["degrees"] = sd["degrees"][: spec.n_degrees]
+    return Problem(name or "custom", sd, pl, hl, f, u0)
+
+
+def eval_basis(p: int, spans: int, x: float, deriv: bool = False):
+    N = np.zeros(p + 1)
+    dN = np.zeros(p + 1)
+    first = _host().iga_eval_basis(p, spans, x, int(deriv), ptr(N), ptr(dN))
+    if first < 0:
+        raise ValueError(_host().iga_last_error().decode())
+    return (first, N, dN) if deriv else (first, N)
+
+
+def geometry_map(geometry: str, patch: int, xi: float, eta: float):
+    X = np.zeros(2)
+    J = np.zeros(4)
+    _check(_host().iga_geometry_map(GEOM[geometry], patch, xi, eta, ptr(X), ptr(J)))
+    return X, J.reshape(2, 2)
