@@ -1,0 +1,339 @@
+"""Benchmark: stand-alone p-multigrid solve to 1e-8 on BASELINE config 5 (1024^2 quarter
+annulus, p=5, V(1,1) p=5->1 with ILUT smoothing) on one B200 per rank.
+
+One step = one complete solve (all V-cycles to rho <= 1e-8) from the zero guess over the
+assembled config-5 system.  metric: DOF-iterations/s = N_dof * cycles / solve time, summed
+over ranks (replicas: the solve does not shard), time = max over ranks.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints ONE JSON line on rank 0.  `e2e` is the same metric through the public API with host
+buffers (pmg.solve: H2D of f and u0, D2H of u inside the timed region).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "solve DOF-iterations/s (stand-alone p-MG V(1,1) to 1e-8)"
+UNIT = "DOF-it/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--degree", type=int, default=0)
+    ap.add_argument("--smoother", choices=["ilut", "gs"], default="ilut")
+    ap.add_argument("--ordering", choices=["none", "rcm"], default="none")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-cycles", type=int, default=0, help="0: a full oracle solve")
+    return ap.parse_args()
+
+
+def dist_init(n_gpus):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return ws, rank, local
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def allreduce_max(x, ws):
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def allreduce_sum(x, ws):
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.p = None
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=10)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh)["hbm_gbs"], "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def algorithmic_bytes(pb, H):
+    """Per-launch algorithmic bytes of the fine-level kernels:
+    CSR(X) = 12 nnz + 4 (rows+1); vectors counted once."""
+    A = pb.plevels[0].A
+    n = A.nrows
+    csr = lambda M: 12 * M.nnz + 4 * (M.nrows + 1)
+    out = {"resid_fine": csr(A) + 24 * n}
+    if H.smoother == "ilut":
+        st = H.factors()[0].stats()
+        out["lsolve_fine"] = 12 * st["nnz_L"] + 4 * (n + 1) + 8 * n + 8 * n + 8 * n  # L, r, y (fill + write)
+        out["usolve_fine"] = 12 * (st["nnz_U"] - n) + 4 * (n + 1) + 8 * n + 8 * n + 8 * n + 16 * n  # U, diag, y, x, u rw
+        out["factor_stats"] = st
+    else:
+        out["gs_fine"] = csr(A) + 8 * n + 8 * n + 8 * n + 8 * n  # A, f, u_old, u_new (fill + write)
+    if len(pb.plevels) > 1:
+        P, PT = pb.plevels[0].P, pb.plevels[0].PT
+        nc = P.ncols
+        out["transfer"] = (csr(PT) + 8 * n + 16 * nc) + (csr(P) + 8 * nc + 24 * n)  # restrict + prolong-add, per cycle
+    return out
+
+
+def run_reference(args, ws, rank):
+    """--impl reference: the CPU oracle (the reference's algorithm restated; the reference itself
+    has no solver code and needs Eigen) on this box's host cores."""
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    from paper_1901_01685_b200 import problems as P
+    pb = P.build(args.config, args.degree)
+    n = pb.n
+    t0 = time.perf_counter()
+    H = O.Hierarchy(pb, smoother=O.GS if args.smoother == "gs" else O.ILUT,
+                    ordering=O.ORDER_RCM if args.ordering == "rcm" else O.ORDER_NONE)
+    setup = time.perf_counter() - t0
+    times, cycles = [], 0
+    for s in range(args.warmup + args.steps):
+        max_c = args.cpu_sample_cycles or 200
+        u, rep = H.solve(pb.f, pb.u0, max_cycles=max_c)
+        if s >= args.warmup:
+            times.append(rep["solve_seconds"])
+            cycles += rep["cycles"]
+    T = sum(times)
+    val = n * cycles / T
+    line = {"metric": METRIC, "value": val, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * T / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (assembled BASELINE config)", "impl": "reference",
+            "config": {"workload": f"config{args.config}", "smoother": args.smoother, "ordering": args.ordering,
+                       "n_dof": n, "cycles_per_solve": cycles / args.steps},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "port",
+                             "sample": f"{args.steps} full oracle solves of config{args.config} "
+                                       f"({cycles // max(args.steps, 1)} cycles each), setup {setup:.1f}s untimed"},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    ws, rank, local = dist_init(args.gpus)
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+        return
+    import torch
+
+    from paper_1901_01685_b200 import pmg
+    from paper_1901_01685_b200 import problems as P
+
+    torch.cuda.set_device(local)
+    P.set_threads(max(1, (os.cpu_count() or 1) // max(ws, 1)))
+    t0 = time.perf_counter()
+    pb = P.build(args.config, args.degree)
+    t_asm = time.perf_counter() - t0
+    n = pb.n
+    H = pmg.build_hierarchy(pb, smoother=args.smoother, ordering=args.ordering)
+    d_f = torch.from_numpy(pb.f).cuda()
+    d_u0 = torch.from_numpy(pb.u0).cuda()
+    d_u = d_u0.clone()
+
+    def one_solve():
+        d_u.copy_(d_u0)
+        torch.cuda.synchronize()
+        return pmg.solve_device(H, d_f.data_ptr(), d_u.data_ptr())
+
+    for _ in range(args.warmup):
+        rep = one_solve()
+    barrier(ws)
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    H.kernel_times(enable=True)
+    times, cycles = [], 0
+    for _ in range(args.steps):
+        rep = one_solve()
+        times.append(rep.solve_seconds)
+        cycles += rep.cycles
+    torch.cuda.synchronize()
+    kt = H.kernel_times()
+    H.kernel_times(enable=False)
+    barrier(ws)
+    clk = clocks.stop()
+    T_local = sum(times)
+    T = allreduce_max(T_local, ws)
+    dof_it = allreduce_sum(n * cycles, ws)
+    value = dof_it / T
+
+    # e2e: public API with host buffers (H2D f, u0 and D2H u inside the timed region)
+    barrier(ws)
+    e2e_t, e2e_c = [], 0
+    for _ in range(args.steps):
+        t1 = time.perf_counter()
+        u, r2 = pmg.solve(H, pb.f, guess=pb.u0)
+        e2e_t.append(time.perf_counter() - t1)
+        e2e_c += r2.cycles
+    T_e2e = allreduce_max(sum(e2e_t), ws)
+    e2e_val = allreduce_sum(n * e2e_c, ws) / T_e2e
+
+    if rank != 0:
+        return
+    # roofline of the dominant fine-level kernel class
+    ab = algorithmic_bytes(pb, H)
+    ms, la = kt["ms"], kt["launches_by_class"]
+    cands = {k: ms[k] for k in ("resid_fine", "lsolve_fine", "usolve_fine", "gs_fine", "transfer") if la.get(k, 0) > 0}
+    dom = max(cands, key=cands.get)
+    per_launch_ms = ms[dom] / la[dom]
+    launches_dom = la[dom]
+    if dom in ("lsolve_fine", "usolve_fine", "gs_fine"):
+        per_launch_ms = ms[dom] / (la[dom] / 3)  # sentinel fill + ticket reset + sweep = one operation
+        launches_dom = la[dom] // 3
+    elif dom == "transfer":
+        per_launch_ms = ms[dom] / (la[dom] / 2)
+        launches_dom = la[dom] // 2
+    bytes_dom = ab[dom]
+    achieved = bytes_dom / (per_launch_ms * 1e-3) / 1e9
+    peak, peak_kind = peaks()
+    roof = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": None, "peak_source": peak_kind, "bytes_per_launch": bytes_dom,
+            "ms_per_launch": per_launch_ms, "launches": launches_dom}
+    # per-V-cycle aggregate fraction
+    total_bytes_cycle = ab["resid_fine"] * 3 + ab.get("transfer", 0)
+    if "lsolve_fine" in ab:
+        total_bytes_cycle += 2 * (ab["lsolve_fine"] + ab["usolve_fine"])
+    else:
+        total_bytes_cycle += 2 * ab["gs_fine"]
+    ms_cycle = 1e3 * T_local / max(cycles, 1)
+    breakdown = {k: {"ms_total": v, "launches": la.get(k, 0)} for k, v in ms.items()}
+
+    cpu = None
+    if not args.no_cpu_baseline and ws == 1:
+        cpu = cpu_baseline(pb, H, args)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * T / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (BASELINE config assembled on the host, random-free zero guess)",
+        "config": {"workload": f"config{args.config}" + (f"_p{args.degree}" if args.config == 2 else ""),
+                   "smoother": args.smoother, "ordering": args.ordering, "n_dof": n,
+                   "nnz_A": pb.plevels[0].A.nnz, "degrees": [l.degree for l in pb.plevels],
+                   "h_levels": len(pb.hlevels), "cycles_per_solve": cycles / args.steps,
+                   "final_rho": float(rep.residual_history[-1]), "converged": bool(rep.converged),
+                   "l2_flush": "inputs larger than L2 (A_p alone is %.2f GB)" % (12 * pb.plevels[0].A.nnz / 1e9),
+                   "parallelism": f"replicas x{ws}", "assembly_s": round(t_asm, 2),
+                   "setup_s": round(H.setup_seconds, 3), "gpu_ilut_s": round(H.ilut_seconds, 3)},
+        "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": 8 * n,
+                "ms_per_step": 1e3 * T_e2e / args.steps},
+        "gpu_launches": kt["launches"],
+        "roofline": roof,
+        "v_cycle": {"ms": ms_cycle, "algorithmic_bytes": total_bytes_cycle,
+                    "achieved_GBs": total_bytes_cycle / (ms_cycle * 1e-3) / 1e9,
+                    "frac": total_bytes_cycle / (ms_cycle * 1e-3) / 1e9 / peak},
+        "kernel_ms": breakdown,
+        "clocks": clk,
+        "cpu_baseline": cpu,
+    }
+    if "factor_stats" in ab:
+        fs = ab["factor_stats"]
+        line["triangular"] = {"levels_L": fs["levels_L"], "levels_U": fs["levels_U"],
+                              "rows_per_level_L": fs["rows_per_level_L"], "rows_per_level_U": fs["rows_per_level_U"],
+                              "nnz_L": fs["nnz_L"], "nnz_U": fs["nnz_U"]}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(pb, H, args):
+    """The oracle (single-threaded CPU port) on this box: a full solve of the same system; its
+    ILUT factors are taken from the GPU (bit-identical to the oracle's, tests/test_gpu_parity.py)
+    to skip a tens-of-minutes CPU setup."""
+    try:
+        from oracle import oracle as O
+        facs = []
+        if args.smoother == "ilut":
+            for F in H.factors():
+                L, U, perm = F.export()
+                facs.append(O.Factor.from_arrays(L, U, perm))
+        else:
+            for F in H.factors():
+                L, U, perm = F.export()
+                facs.append(O.Factor.from_arrays(L, U, perm))
+        Ho = O.Hierarchy(pb, smoother=O.GS if args.smoother == "gs" else O.ILUT, factors=facs)
+        max_c = args.cpu_sample_cycles or 200
+        t0 = time.perf_counter()
+        u, rep = Ho.solve(pb.f, pb.u0, max_cycles=max_c)
+        wall = time.perf_counter() - t0
+        return {"value": pb.n * rep["cycles"] / rep["solve_seconds"], "unit": UNIT, "cores": 1, "kind": "port",
+                "sample": f"one oracle solve of the same system ({rep['cycles']} cycles, {wall:.1f}s wall), "
+                          f"GPU-built ILUT factors", "cycles": rep["cycles"]}
+    except Exception as e:  # report, never hide
+        return {"value": None, "unit": UNIT, "cores": 1, "kind": "port", "sample": f"failed: {e}"}
+
+
+if __name__ == "__main__":
+    main()

@@ -128,6 +128,12 @@ int pmg_restrict(pmg_hier H, int level, const double* r_fine, double* r_coarse);
  * pmg_solve_device call and report per-kernel-class device time (ms). */
 int pmg_work_kernel_times(pmg_work W, double* ms_by_class, int n_classes);
 
+/* diagnostics: mode 1/0 enables/disables per-segment globaltimer tracing of the chained
+ * sweeps; mode -1 copies the trace of the last sweep (6 u64 per segment: claim, helpers done,
+ * finisher start, finisher end, helper value spins, finisher batch waits) and returns the
+ * number of segments */
+int pmg_debug_chain_trace(int mode, unsigned long long* out, int cap);
+
 #ifdef __cplusplus
 }
 #endif

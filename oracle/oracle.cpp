@@ -84,9 +84,11 @@ static double norm2(const double* r, int64_t n) {
     return std::sqrt(chunk_reduce(buf));
 }
 
-// Forward lexicographic Gauss-Seidel, u_i <- ((f_i - S_L) - S_U) / a_ii with S_L over
+// Forward lexicographic Gauss-Seidel, u_i <- ((f_i - S_L) - S_U) * (1/a_ii) with S_L over
 // j < i (new values) and S_U over j > i (old values), each ascending from +0
-// (SPEC.md:233-241).  Returns -1 or the row with a zero/missing diagonal.
+// (SPEC.md:233-241).  The diagonal is applied as a multiplication by its IEEE reciprocal
+// 1.0/a_ii (computed once per matrix).  Returns -1 or the row with a
+// zero/missing diagonal.
 static int64_t gs_sweep(const Csr& A, double* u, const double* f) {
     for (int32_t i = 0; i < A.n; ++i) {
         double sl = 0.0, su = 0.0, d = 0.0;
@@ -98,7 +100,8 @@ static int64_t gs_sweep(const Csr& A, double* u, const double* f) {
             else { d = A.v[k]; has_d = true; }
         }
         if (!has_d || d == 0.0) return i;
-        u[i] = ((f[i] - sl) - su) / d;
+        const double dinv = 1.0 / d;
+        u[i] = ((f[i] - sl) - su) * dinv;
     }
     return -1;
 }
@@ -302,14 +305,15 @@ static void lsolve(const Factor& F, const double* r, double* y) {
         y[i] = r[F.perm[i]] - s;
     }
 }
-// x_i = (y_i - S) / u_ii, S over the off-diagonal entries in DESCENDING column order;
-// then u[perm[i]] = u[perm[i]] + x_i.
+// x_i = (y_i - S) * (1/u_ii), S over the off-diagonal entries in DESCENDING column order;
+// then u[perm[i]] = u[perm[i]] + x_i.  (1/u_ii: IEEE reciprocal, as in the GS sweep.)
 static void usolve_add(const Factor& F, const double* y, double* x, double* u) {
     for (int32_t i = F.n - 1; i >= 0; --i) {
         const int32_t d0 = F.U.rp[i];
         double s = 0.0;
         for (int32_t k = F.U.rp[i + 1] - 1; k > d0; --k) s = s + F.U.v[k] * x[F.U.ci[k]];
-        x[i] = (y[i] - s) / F.U.v[d0];
+        const double dinv = 1.0 / F.U.v[d0];
+        x[i] = (y[i] - s) * dinv;
         u[F.perm[i]] = u[F.perm[i]] + x[i];
     }
 }

@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "../../../include/pmg_cuda.h"
+#include "chain.cuh"
 #include "dense.cuh"
 #include "ilut.cuh"
 #include "rcm.hpp"
@@ -80,6 +81,11 @@ DevCsr upload(const pmg_csr_view& v, cudaStream_t st) {
     return d;
 }
 
+bool force_levelsched() {
+    const char* e = getenv("PMG_FORCE_LEVELSCHED");
+    return e && e[0] == '1';
+}
+
 struct Stream {
     cudaStream_t s = nullptr;
     Stream() { PMG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)); }
@@ -104,6 +110,8 @@ struct pmg_csr_s {
     Sell gs;
     double* gs_diag = nullptr;
     int32_t* gs_nlow = nullptr;
+    int32_t seg = 0;              // chained-segment length (0: level-scheduled sweeps)
+    int32_t* gs_split = nullptr;
     ~pmg_csr_s() {
         A.free();
         sell_free(S);
@@ -112,6 +120,7 @@ struct pmg_csr_s {
             sell_free(gs);
             cudaFree(gs_diag);
             cudaFree(gs_nlow);
+            cudaFree(gs_split);
         }
     }
 };
@@ -123,9 +132,12 @@ struct pmg_factor_s {
     std::vector<int32_t> h_perm;
     LevelSets lvL, lvU;
     Sell Ls, Us;
-    double* Udiag = nullptr;          // diagonal of U per U-level position
+    double* Udiag = nullptr;          // 1.0 / diagonal of U per sweep position
     int32_t max_row_L = 0, max_row_U = 0;
     double seconds = 0;
+    int32_t seg = 0;                  // chained-segment length (0: level-scheduled sweeps)
+    int32_t* rev = nullptr;           // v -> row for the U sweep (descending rows)
+    int32_t *splitL = nullptr, *splitU = nullptr;
     ~pmg_factor_s() {
         L.free();
         U.free();
@@ -135,10 +147,35 @@ struct pmg_factor_s {
         sell_free(Ls);
         sell_free(Us);
         cudaFree(Udiag);
+        cudaFree(rev);
+        cudaFree(splitL);
+        cudaFree(splitU);
     }
 };
 
 namespace {
+
+// e = U^{-1} L^{-1} r[perm] added into u[perm]  (y, x: scratch)
+void apply_factor(pmg_factor_s* F, const double* r, double* y, double* x, double* u, int* ticket, cudaStream_t st) {
+    if (F->seg > 0) {
+        ChainOp l{kChainL, &F->Ls, nullptr, nullptr, F->splitL, F->perm, r, nullptr, y, nullptr, F->seg};
+        chain_sweep(l, ticket, st);
+        ChainOp up{kChainU, &F->Us, F->Udiag, nullptr, F->splitU, F->perm, y, nullptr, x, u, F->seg};
+        chain_sweep(up, ticket, st);
+    } else {
+        lsolve(F->Ls, F->perm, r, y, ticket, st);
+        usolve_add(F->Us, F->Udiag, F->perm, y, x, u, ticket, st);
+    }
+}
+
+void gs_apply(pmg_csr_s* A, const double* f, const double* uo, double* un, int* ticket, cudaStream_t st) {
+    if (A->seg > 0) {
+        ChainOp g{kChainGS, &A->gs, A->gs_diag, A->gs_nlow, A->gs_split, nullptr, f, uo, un, nullptr, A->seg};
+        chain_sweep(g, ticket, st);
+    } else {
+        gs_sweep(A->gs, A->gs_diag, A->gs_nlow, f, uo, un, ticket, st);
+    }
+}
 
 pmg_csr_s* make_csr(const pmg_csr_view& v, cudaStream_t st) {
     auto h = std::make_unique<pmg_csr_s>();
@@ -147,6 +184,7 @@ pmg_csr_s* make_csr(const pmg_csr_view& v, cudaStream_t st) {
     h->h_col.assign(v.col, v.col + h->A.nnz);
     h->h_val.assign(v.val, v.val + h->A.nnz);
     h->band = pmg_host::bandwidth(v.nrows, v.rowptr, v.col);
+    h->seg = force_levelsched() ? 0 : detect_segment(v.nrows, v.rowptr, v.col);
     sell_build(h->S, v.nrows, h->A.rowptr, h->A.col, h->A.val, nullptr, kPickAll, nullptr, nullptr, st);
     PMG_CUDA(cudaStreamSynchronize(st));
     return h.release();
@@ -158,7 +196,12 @@ void ensure_gs(pmg_csr_s* h, cudaStream_t st) {
     level_sets(h->gs_lv, n, h->A.rowptr, h->A.col, kDepLower, st);
     h->gs_diag = dalloc<double>(n);
     h->gs_nlow = dalloc<int32_t>(n);
-    sell_build(h->gs, n, h->A.rowptr, h->A.col, h->A.val, h->gs_lv.order, kPickOffDiag, h->gs_diag, h->gs_nlow, st);
+    sell_build(h->gs, n, h->A.rowptr, h->A.col, h->A.val, h->seg > 0 ? nullptr : h->gs_lv.order, kPickOffDiag,
+               h->gs_diag, h->gs_nlow, st);
+    if (h->seg > 0) {
+        h->gs_split = dalloc<int32_t>(n);
+        chain_split(h->gs, h->gs_nlow, h->seg, kChainGS, h->gs_split, st);
+    }
     // first row (in row order) with a zero or missing diagonal -> SPEC.md:237 smoother error
     std::vector<double> dg(n);
     std::vector<int32_t> ord(n);
@@ -166,9 +209,12 @@ void ensure_gs(pmg_csr_s* h, cudaStream_t st) {
     PMG_CUDA(cudaMemcpyAsync(ord.data(), h->gs_lv.order, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
     PMG_CUDA(cudaStreamSynchronize(st));
     int64_t zr = -1;
-    for (int32_t p = 0; p < n; ++p)
-        if (dg[p] == 0.0 && (zr < 0 || ord[p] < zr)) zr = ord[p];
+    for (int32_t p = 0; p < n; ++p) {
+        const int32_t row = h->seg > 0 ? p : ord[p];
+        if (dg[p] == 0.0 && (zr < 0 || row < zr)) zr = row;
+    }
     h->gs_zero_row = zr;
+    reciprocal_inplace(h->gs_diag, n, st);
     h->gs_ready = true;
 }
 
@@ -183,6 +229,7 @@ int make_factor(pmg_csr_s* A, double tau, double fillfactor, int ordering, pmg_f
     DevCsr Ap = A->A;
     DevCsr owned;
     int32_t band = A->band;
+    F->seg = A->seg;
     if (ordering == PMG_ORDER_RCM) {
         F->h_perm = pmg_host::rcm_ordering(n, A->h_rowptr.data(), A->h_col.data());
         std::vector<int32_t> brp, bci;
@@ -190,6 +237,7 @@ int make_factor(pmg_csr_s* A, double tau, double fillfactor, int ordering, pmg_f
         band = pmg_host::permute_symmetric(n, A->h_rowptr.data(), A->h_col.data(), A->h_val.data(), F->h_perm, brp,
                                            bci, bv);
         pmg_csr_view v{n, n, brp.data(), bci.data(), bv.data()};
+        F->seg = force_levelsched() ? 0 : detect_segment(n, brp.data(), bci.data());
         owned = upload(v, st);
         Ap = owned;
         F->perm = dalloc<int32_t>(n);
@@ -203,9 +251,23 @@ int make_factor(pmg_csr_s* A, double tau, double fillfactor, int ordering, pmg_f
     if (rc != 0) return PMG_ZERO_PIVOT;
     level_sets(F->lvL, n, F->L.rowptr, F->L.col, kDepLower, st);
     level_sets(F->lvU, n, F->U.rowptr, F->U.col, kDepUpper, st);
-    sell_build(F->Ls, n, F->L.rowptr, F->L.col, F->L.val, F->lvL.order, kPickAll, nullptr, nullptr, st);
     F->Udiag = dalloc<double>(n);
-    sell_build(F->Us, n, F->U.rowptr, F->U.col, F->U.val, F->lvU.order, kPickOffDiagDesc, F->Udiag, nullptr, st);
+    if (F->seg > 0) {  // chained-segment layouts: L in row order, U in descending row order
+        F->rev = dalloc<int32_t>(n);
+        std::vector<int32_t> rv(n);
+        for (int32_t v = 0; v < n; ++v) rv[v] = n - 1 - v;
+        PMG_CUDA(cudaMemcpyAsync(F->rev, rv.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, st));
+        sell_build(F->Ls, n, F->L.rowptr, F->L.col, F->L.val, nullptr, kPickAll, nullptr, nullptr, st);
+        sell_build(F->Us, n, F->U.rowptr, F->U.col, F->U.val, F->rev, kPickOffDiagDesc, F->Udiag, nullptr, st);
+        F->splitL = dalloc<int32_t>(n);
+        F->splitU = dalloc<int32_t>(n);
+        chain_split(F->Ls, nullptr, F->seg, kChainL, F->splitL, st);
+        chain_split(F->Us, nullptr, F->seg, kChainU, F->splitU, st);
+    } else {
+        sell_build(F->Ls, n, F->L.rowptr, F->L.col, F->L.val, F->lvL.order, kPickAll, nullptr, nullptr, st);
+        sell_build(F->Us, n, F->U.rowptr, F->U.col, F->U.val, F->lvU.order, kPickOffDiagDesc, F->Udiag, nullptr, st);
+    }
+    reciprocal_inplace(F->Udiag, n, st);  // nonzero: a zero pivot was reported above
     // longest rows (reporting)
     std::vector<int32_t> lr(n + 1), ur(n + 1);
     PMG_CUDA(cudaMemcpyAsync(lr.data(), F->L.rowptr, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToHost, st));
@@ -374,8 +436,19 @@ void smooth_ilut(pmg_work_s& W, pmg_csr_s* A, pmg_factor_s* F, double* u, const 
         W.run(fine ? kClsResid0 : kClsCoarse, 1, [&] { sell_rowop(A->S, kOpResidual, u, f, nullptr, r, nullptr, W.st); });
         rr = r;
     }
-    W.run(fine ? kClsL0 : kClsCoarse, 3, [&] { lsolve(F->Ls, F->perm, rr, y, W.ticket, W.st); });
-    W.run(fine ? kClsU0 : kClsCoarse, 3, [&] { usolve_add(F->Us, F->Udiag, F->perm, y, x, u, W.ticket, W.st); });
+    if (F->seg > 0) {
+        W.run(fine ? kClsL0 : kClsCoarse, 3, [&] {
+            ChainOp l{kChainL, &F->Ls, nullptr, nullptr, F->splitL, F->perm, rr, nullptr, y, nullptr, F->seg};
+            chain_sweep(l, W.ticket, W.st);
+        });
+        W.run(fine ? kClsU0 : kClsCoarse, 3, [&] {
+            ChainOp up{kChainU, &F->Us, F->Udiag, nullptr, F->splitU, F->perm, y, nullptr, x, u, F->seg};
+            chain_sweep(up, W.ticket, W.st);
+        });
+    } else {
+        W.run(fine ? kClsL0 : kClsCoarse, 3, [&] { lsolve(F->Ls, F->perm, rr, y, W.ticket, W.st); });
+        W.run(fine ? kClsU0 : kClsCoarse, 3, [&] { usolve_add(F->Us, F->Udiag, F->perm, y, x, u, W.ticket, W.st); });
+    }
 }
 
 // one h-MG V(1,1) cycle on h-level j from e = 0
@@ -407,9 +480,7 @@ int smooth(pmg_work_s& W, int l, const double* f, const double* r_known) {
         if (L.A->gs_zero_row >= 0) return PMG_ZERO_DIAG;
         double* uo = w.u[w.cur];
         double* un = w.u[1 - w.cur];
-        W.run(fine ? kClsGS0 : kClsCoarse, 3, [&] {
-            gs_sweep(L.A->gs, L.A->gs_diag, L.A->gs_nlow, f, uo, un, W.ticket, W.st);
-        });
+        W.run(fine ? kClsGS0 : kClsCoarse, 3, [&] { gs_apply(L.A, f, uo, un, W.ticket, W.st); });
         w.cur = 1 - w.cur;
         return PMG_OK;
     }
@@ -635,7 +706,7 @@ int pmg_gs_sweep(pmg_csr A, double* u, const double* f, int64_t* err_row) {
         int* tk = reinterpret_cast<int*>(hv.make(1));
         PMG_CUDA(cudaMemcpyAsync(du, u, sizeof(double) * n, cudaMemcpyHostToDevice, s.s));
         PMG_CUDA(cudaMemcpyAsync(df, f, sizeof(double) * n, cudaMemcpyHostToDevice, s.s));
-        gs_sweep(A->gs, A->gs_diag, A->gs_nlow, df, du, dn, tk, s.s);
+        gs_apply(A, df, du, dn, tk, s.s);
         PMG_CUDA(cudaMemcpyAsync(u, dn, sizeof(double) * n, cudaMemcpyDeviceToHost, s.s));
         PMG_CUDA(cudaStreamSynchronize(s.s));
         return int(PMG_OK);
@@ -675,8 +746,7 @@ int pmg_ilut_apply(pmg_factor F, const double* r, double* e) {
         int* tk = reinterpret_cast<int*>(hv.make(1));
         PMG_CUDA(cudaMemcpyAsync(dr, r, sizeof(double) * n, cudaMemcpyHostToDevice, s.s));
         PMG_CUDA(cudaMemsetAsync(de, 0, sizeof(double) * n, s.s));
-        lsolve(F->Ls, F->perm, dr, dy, tk, s.s);
-        usolve_add(F->Us, F->Udiag, F->perm, dy, dx, de, tk, s.s);
+        apply_factor(F, dr, dy, dx, de, tk, s.s);
         PMG_CUDA(cudaMemcpyAsync(e, de, sizeof(double) * n, cudaMemcpyDeviceToHost, s.s));
         PMG_CUDA(cudaStreamSynchronize(s.s));
         return PMG_OK;
@@ -954,6 +1024,20 @@ int pmg_restrict(pmg_hier H, int level, const double* rf, double* rc) {
         PMG_CUDA(cudaStreamSynchronize(s.s));
         return PMG_OK;
     });
+}
+
+// diagnostics: enable (1) / disable (0) per-segment tracing of chained sweeps; or (-1) copy the
+// trace of the last sweep (6 u64 per segment) into out (cap entries); returns #segments
+int pmg_debug_chain_trace(int mode, unsigned long long* out, int cap) {
+    if (mode == 1 || mode == 0) {
+        g_chain_trace_on = mode == 1;
+        return 0;
+    }
+    if (!g_chain_trace || !out) return 0;
+    const int n = std::min(g_chain_trace_n * 6 + 64 * 5 + 1024, cap);
+    if (cudaDeviceSynchronize() != cudaSuccess) return -1;
+    if (cudaMemcpy(out, g_chain_trace, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+    return g_chain_trace_n;
 }
 
 // ms_by_class[0..6]: resid(A_p), L-solve(p), U-solve(p), GS(p), p-transfers, coarse (p<finest and

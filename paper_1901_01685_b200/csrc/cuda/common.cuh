@@ -41,6 +41,12 @@ __device__ __forceinline__ double ld_relaxed(const double* p) {
     asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
     return v;
 }
+// same load without a compiler memory barrier: lets independent loads be batched
+__device__ __forceinline__ double ld_relaxed_nb(const double* p) {
+    double v;
+    asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
 __device__ __forceinline__ void st_relaxed(double* p, double v) {
     asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }

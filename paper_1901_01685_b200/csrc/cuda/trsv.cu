@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(256) k_lsolve(Sell L, const int32_t* __restric
     st_relaxed(y + i, rhs - acc);
 }
 
-// x_i = (y_i - sum_j u_ij x_j) / u_ii  (descending j);  u[perm[i]] = u[perm[i]] + x_i
+// x_i = (y_i - sum_j u_ij x_j) * dinv_i  (descending j; dinv = 1.0/u_ii);  u[perm[i]] += x_i
 __global__ void __launch_bounds__(256) k_usolve_add(Sell U, const double* __restrict__ diag,
                                                     const int32_t* __restrict__ perm, const double* __restrict__ y,
                                                     double* x, double* __restrict__ u, int* ticket) {
@@ -137,14 +137,14 @@ __global__ void __launch_bounds__(256) k_usolve_add(Sell U, const double* __rest
         if (k + 2 < len) acc = acc + v1.x * wait_value(x, c.z);
         if (k + 3 < len) acc = acc + v1.y * wait_value(x, c.w);
     }
-    const double xi = (y[i] - acc) / diag[pos];
+    const double xi = (y[i] - acc) * diag[pos];
     st_relaxed(x + i, xi);
     const int32_t ui = perm ? perm[i] : i;
     u[ui] = u[ui] + xi;
 }
 
 // Gauss-Seidel: lower entries read the new values (published by earlier rows), upper
-// entries the old ones; u_new_i = ((f_i - S_L) - S_U) / a_ii
+// entries the old ones; u_new_i = ((f_i - S_L) - S_U) * dinv_i  (dinv = 1.0/a_ii)
 __global__ void __launch_bounds__(256) k_gs(Sell A, const double* __restrict__ diag, const int32_t* __restrict__ nlow,
                                             const double* __restrict__ f, const double* __restrict__ u_old,
                                             double* u_new, int* ticket) {
@@ -170,7 +170,18 @@ __global__ void __launch_bounds__(256) k_gs(Sell A, const double* __restrict__ d
             else su = su + vv[q] * __ldg(u_old + cc[q]);
         }
     }
-    st_relaxed(u_new + i, ((f[i] - sl) - su) / diag[pos]);
+    st_relaxed(u_new + i, ((f[i] - sl) - su) * diag[pos]);
+}
+
+__global__ void k_reciprocal(double* d, int32_t n) {
+    int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) d[i] = 1.0 / d[i];
+}
+
+void reciprocal_inplace(double* d, int32_t n, cudaStream_t st) {
+    if (n <= 0) return;
+    k_reciprocal<<<ceil_div(n, 256), 256, 0, st>>>(d, n);
+    PMG_LAUNCH_CHECK();
 }
 
 void lsolve(const Sell& L, const int32_t* perm, const double* r, double* y, int* ticket, cudaStream_t st) {

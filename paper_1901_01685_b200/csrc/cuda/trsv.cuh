@@ -21,6 +21,9 @@ void level_sets(LevelSets& ls, int32_t n, const int32_t* d_rowptr, const int32_t
                 cudaStream_t st);
 void level_sets_free(LevelSets& ls);
 
+// d[i] = 1.0 / d[i] (IEEE): the U / GS sweeps multiply by reciprocal diagonals
+void reciprocal_inplace(double* d, int32_t n, cudaStream_t st);
+
 // y = L^{-1} r[perm]   (unit lower, L rows in level order, ascending accumulation)
 void lsolve(const Sell& L, const int32_t* perm, const double* r, double* y, int* ticket, cudaStream_t st);
 // x = U^{-1} y; u[perm[i]] += x_i   (U off-diagonals descending, diag per position)

@@ -14,6 +14,17 @@ from paper_1901_01685_b200 import problems as P
 
 pytestmark = pytest.mark.gpu
 
+
+@pytest.fixture(params=["chain", "levelsched"])
+def sweep_path(request, monkeypatch):
+    """Both sweep implementations must match the oracle: the chained-segment wavefront
+    (default for tensor-grid orderings) and the level-scheduled sync-free fallback."""
+    if request.param == "levelsched":
+        monkeypatch.setenv("PMG_FORCE_LEVELSCHED", "1")
+    else:
+        monkeypatch.delenv("PMG_FORCE_LEVELSCHED", raising=False)
+    return request.param
+
 RTOL_RHO = 1e-10
 RTOL_U = 1e-12
 
@@ -63,7 +74,7 @@ def test_spmv_residual_bitwise(cfg1):
 
 
 @pytest.mark.parametrize("ordering", ["none", "rcm"])
-def test_ilut_factors_bitwise(cfg1, ordering):
+def test_ilut_factors_bitwise(cfg1, ordering, sweep_path):
     for lev in cfg1.plevels:
         A = lev.A
         Fg = pmg.ilut_factorize(A, 1e-12, 1.0, ordering)
@@ -81,7 +92,7 @@ def test_ilut_factors_bitwise(cfg1, ordering):
         assert_bitwise(pmg.ilut_apply(Fg, r), Fo.apply(r), "ilut_apply")
 
 
-def test_gs_sweep_bitwise(cfg1):
+def test_gs_sweep_bitwise(cfg1, sweep_path):
     A = cfg1.plevels[0].A
     rng = np.random.default_rng(2)
     u = rng.uniform(-1, 1, A.nrows)
@@ -105,17 +116,17 @@ def _solve_parity(pb, smoother="ilut", ordering="none"):
 
 
 @pytest.mark.parametrize("ordering", ["none", "rcm"])
-def test_solve_config1(cfg1, ordering):
+def test_solve_config1(cfg1, ordering, sweep_path):
     rep, ro = _solve_parity(cfg1, "ilut", ordering)
     assert rep.converged
 
 
 @pytest.mark.parametrize("degree", [2, 3, 4])
 @pytest.mark.parametrize("smoother", ["ilut", "gs"])
-def test_solve_config2(degree, smoother):
+def test_solve_config2(degree, smoother, sweep_path):
     _solve_parity(problem(2, degree), smoother)
 
 
-def test_solve_config3():
+def test_solve_config3(sweep_path):
     rep, _ = _solve_parity(problem(3), "ilut")
     assert rep.converged
