@@ -59,6 +59,11 @@ int iga_problem_csr_copy(const iga_problem* h, int kind, int l, int32_t* rowptr,
 int iga_problem_vec_len(const iga_problem* h, int kind, int l);
 int iga_problem_vec_copy(const iga_problem* h, int kind, int l, double* out);
 
+/* one operator on one space: kind 0 = CDR operator A (load f=1 in IGA_VEC_F), 1 = mass M,
+ * 2 = transfer P^p_{p2}, 3 = mass + lumped mass (IGA_VEC_ML); read it back as p-level 0 */
+int iga_matrix_build(int kind, int geometry, int p, int p2, int nel, const double* D, const double* v, double R,
+                     double nitsche_scale, iga_problem** out);
+
 /* SPEC.md:61-78 and :79-87 (used by the property tests) */
 int iga_eval_basis(int p, int spans, double x, int with_deriv, double* N, double* dN);
 int iga_geometry_map(int geometry, int patch, double xi, double eta, double* X, double* J);

@@ -6,6 +6,7 @@
 #include "oracle.h"
 
 #include <algorithm>
+#include <climits>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -14,7 +15,26 @@
 #include <string>
 #include <vector>
 
+#include <atomic>
+#include <thread>
+
 namespace orc {
+
+// ---- host threads (test infrastructure speed only; every row's arithmetic is unchanged) ----
+static int g_threads = 1;
+template <class F>
+static void par_rows(int32_t n, F&& body) {  // body(i0, i1) over disjoint row blocks
+    const int nt = std::max(1, std::min(g_threads, int((n + 4095) / 4096)));
+    if (nt == 1) {
+        body(0, n);
+        return;
+    }
+    std::vector<std::thread> th;
+    const int32_t chunk = (n + nt - 1) / nt;
+    for (int t = 0; t < nt; ++t)
+        th.emplace_back([&, t] { body(std::min(n, t * chunk), std::min(n, (t + 1) * chunk)); });
+    for (auto& x : th) x.join();
+}
 
 struct Csr {
     int32_t n = 0, m = 0;
@@ -39,12 +59,11 @@ static inline double row_dot(const int32_t* rp, const int32_t* ci, const double*
     return s;
 }
 
-static void spmv(const Csr& A, const double* x, double* y) {
-    for (int32_t i = 0; i < A.n; ++i) y[i] = row_dot(A.rp.data(), A.ci.data(), A.v.data(), i, x);
-}
 // r_i = f_i - (A x)_i
 static void residual(const Csr& A, const double* x, const double* f, double* r) {
-    for (int32_t i = 0; i < A.n; ++i) r[i] = f[i] - row_dot(A.rp.data(), A.ci.data(), A.v.data(), i, x);
+    par_rows(A.n, [&](int32_t i0, int32_t i1) {
+        for (int32_t i = i0; i < i1; ++i) r[i] = f[i] - row_dot(A.rp.data(), A.ci.data(), A.v.data(), i, x);
+    });
 }
 
 // ||r||_2 in the canonical blocked order: chunks of 256 entries; inside a chunk eight
@@ -204,6 +223,107 @@ static void keep_largest(std::vector<Cand>& c, int32_t M) {
 //     w_j = w_j - w_k * u_kj for the off-diagonal entries of U row k;
 //   U entries with |w_j| < tau_i dropped; rule 2 keeps the M = ceil(m nnz/n) largest in L and in U
 //   (diagonal always kept); zero diagonal -> error(row).
+namespace {
+struct RowOut {  // one factor row: L part (ascending) or U part (diagonal first, then ascending)
+    std::vector<int32_t> c;
+    std::vector<double> v;
+};
+struct IlutScratch {
+    std::vector<double> w;
+    std::vector<char> present;
+    std::vector<uint64_t> bits;
+    std::vector<std::pair<int32_t, double>> row;
+    std::vector<int32_t> upos, touched;
+    std::vector<Cand> lc, uc;
+    explicit IlutScratch(int32_t n) : w(n, 0.0), present(n, 0), bits(size_t(n) / 64 + 2, 0) {}
+};
+}  // namespace
+
+// one row of the IKJ elimination; U rows of earlier rows are read once their `done` flag is set
+static bool ilut_row(int32_t i, const pmg_csr_view& A, const std::vector<int32_t>& perm,
+                     const std::vector<int32_t>& pinv, double tau, int32_t M, std::vector<RowOut>& Lr,
+                     std::vector<RowOut>& Ur, std::atomic<int>* done, IlutScratch& S) {
+    std::vector<double>& w = S.w;
+    std::vector<char>& present = S.present;
+    std::vector<uint64_t>& bits = S.bits;
+    const int32_t old = perm[i];
+    S.row.clear();
+    for (int32_t k = A.rowptr[old]; k < A.rowptr[old + 1]; ++k) S.row.push_back({pinv[A.col[k]], A.val[k]});
+    std::sort(S.row.begin(), S.row.end());
+    double asum = 0.0;
+    for (auto& e : S.row) asum = asum + std::fabs(e.second);
+    const double tau_i = tau * (asum / double(S.row.size()));
+    S.upos.clear();
+    S.touched.clear();
+    int32_t kmin = i;
+    for (auto& e : S.row) {
+        int32_t c = e.first;
+        w[c] = e.second;
+        present[c] = 1;
+        S.touched.push_back(c);
+        if (c < i) { bits[c >> 6] |= 1ull << (c & 63); kmin = std::min(kmin, c); }
+        else if (c > i) S.upos.push_back(c);
+    }
+    S.lc.clear();
+    // ascending pivot scan over the L-part bitmap
+    int32_t k = kmin;
+    while (k < i) {
+        int64_t wi = k >> 6;
+        uint64_t word = bits[wi] & (~0ull << (k & 63));
+        while (word == 0 && (wi + 1) * 64 < int64_t(i)) word = bits[++wi];
+        if (word == 0) break;
+        k = int32_t(wi * 64 + __builtin_ctzll(word));
+        if (k >= i) break;
+        bits[k >> 6] &= ~(1ull << (k & 63));
+        while (done[k].load(std::memory_order_acquire) == 0) std::this_thread::yield();
+        const RowOut& Uk = Ur[k];
+        const double wk = w[k] / Uk.v[0];
+        if (std::fabs(wk) < tau_i) {
+            w[k] = 0.0;
+            present[k] = 0;
+        } else {
+            w[k] = wk;
+            S.lc.push_back({k, wk});
+            for (size_t q = 1; q < Uk.c.size(); ++q) {
+                int32_t j = Uk.c[q];
+                if (!present[j]) {
+                    present[j] = 1;
+                    S.touched.push_back(j);
+                    if (j < i) bits[j >> 6] |= 1ull << (j & 63);
+                    else if (j > i) S.upos.push_back(j);
+                }
+                w[j] = w[j] - wk * Uk.v[q];
+            }
+        }
+        ++k;
+    }
+    const double diag = present[i] ? w[i] : 0.0;
+    bool ok = diag != 0.0;
+    S.uc.clear();
+    for (int32_t j : S.upos)
+        if (!(std::fabs(w[j]) < tau_i)) S.uc.push_back({j, w[j]});
+    keep_largest(S.lc, M);
+    keep_largest(S.uc, M);
+    RowOut& L = Lr[i];
+    RowOut& U = Ur[i];
+    for (auto& e : S.lc) { L.c.push_back(e.c); L.v.push_back(e.v); }
+    U.c.push_back(i);
+    U.v.push_back(ok ? diag : 1.0);  // 1.0 only keeps later rows running; the error is reported
+    for (auto& e : S.uc) { U.c.push_back(e.c); U.v.push_back(e.v); }
+    for (int32_t c : S.touched) { w[c] = 0.0; present[c] = 0; }
+    done[i].store(1, std::memory_order_release);
+    return ok;
+}
+
+// Dual-threshold ILUT(tau, m), IKJ on the symmetrically permuted matrix (SPEC.md:251-259,
+// PAPER.md:298-311):
+//   tau_i = tau * (sum_j |a_ij| / nnz_i) over the permuted row's stored entries (ascending column);
+//   pivots k ascending (including fill): w_k = w_k / u_kk; drop if |w_k| < tau_i (rule 1), else
+//     w_j = w_j - w_k * u_kj for the off-diagonal entries of U row k;
+//   U entries with |w_j| < tau_i dropped; rule 2 keeps the M = ceil(m nnz/n) largest in L and in U
+//   (diagonal always kept); zero diagonal -> error(row).
+// Rows may be processed by several host threads (rows claimed in ascending order, each waits for
+// the U rows it pivots on); every row's arithmetic is the sequential algorithm's.
 static std::unique_ptr<Factor> ilut(const pmg_csr_view& A, double tau, double m, int ordering, int64_t* err_row) {
     const int32_t n = A.nrows;
     auto F = std::make_unique<Factor>();
@@ -215,83 +335,53 @@ static std::unique_ptr<Factor> ilut(const pmg_csr_view& A, double tau, double m,
     for (int32_t i = 0; i < n; ++i) F->pinv[F->perm[i]] = i;
     const int64_t nnz = A.rowptr[n];
     const int32_t M = int32_t(std::ceil(m * double(nnz) / double(n)));
+    std::vector<RowOut> Lr(n), Ur(n);
+    std::unique_ptr<std::atomic<int>[]> done(new std::atomic<int>[n]);
+    for (int32_t i = 0; i < n; ++i) done[i].store(0, std::memory_order_relaxed);
+    std::atomic<int32_t> next{0}, first_bad{INT32_MAX};
+    auto worker = [&] {
+        IlutScratch S(n);
+        for (;;) {
+            const int32_t i = next.fetch_add(1);
+            if (i >= n) break;
+            if (!ilut_row(i, A, F->perm, F->pinv, tau, M, Lr, Ur, done.get(), S)) {
+                int32_t cur = first_bad.load();
+                while (i < cur && !first_bad.compare_exchange_weak(cur, i)) {
+                }
+            }
+        }
+    };
+    const int nt = std::max(1, std::min(g_threads, int(n / 256) + 1));
+    if (nt == 1) worker();
+    else {
+        std::vector<std::thread> th;
+        for (int t = 0; t < nt; ++t) th.emplace_back(worker);
+        for (auto& x : th) x.join();
+    }
+    if (first_bad.load() != INT32_MAX) {
+        if (err_row) *err_row = first_bad.load();
+        return nullptr;
+    }
     F->L.n = F->L.m = F->U.n = F->U.m = n;
     F->L.rp.assign(n + 1, 0);
     F->U.rp.assign(n + 1, 0);
-    std::vector<double> w(n, 0.0);
-    std::vector<char> present(n, 0);
-    std::vector<uint64_t> bits(size_t(n) / 64 + 2, 0);
-    std::vector<std::pair<int32_t, double>> row;
-    std::vector<int32_t> upos, touched;
-    std::vector<Cand> lc, uc;
     for (int32_t i = 0; i < n; ++i) {
-        int32_t old = F->perm[i];
-        row.clear();
-        for (int32_t k = A.rowptr[old]; k < A.rowptr[old + 1]; ++k) row.push_back({F->pinv[A.col[k]], A.val[k]});
-        std::sort(row.begin(), row.end());
-        double asum = 0.0;
-        for (auto& e : row) asum = asum + std::fabs(e.second);
-        const double tau_i = tau * (asum / double(row.size()));
-        upos.clear();
-        touched.clear();
-        int32_t kmin = i;
-        for (auto& e : row) {
-            int32_t c = e.first;
-            w[c] = e.second;
-            present[c] = 1;
-            touched.push_back(c);
-            if (c < i) { bits[c >> 6] |= 1ull << (c & 63); kmin = std::min(kmin, c); }
-            else if (c > i) upos.push_back(c);
-        }
-        lc.clear();
-        // ascending pivot scan over the L-part bitmap
-        int32_t k = kmin;
-        while (k < i) {
-            int64_t wi = k >> 6;
-            uint64_t word = bits[wi] & (~0ull << (k & 63));
-            while (word == 0 && (wi + 1) * 64 < int64_t(i)) word = bits[++wi];
-            if (word == 0) break;
-            k = int32_t(wi * 64 + __builtin_ctzll(word));
-            if (k >= i) break;
-            bits[k >> 6] &= ~(1ull << (k & 63));
-            const int32_t d0 = F->U.rp[k];
-            const double wk = w[k] / F->U.v[d0];
-            if (std::fabs(wk) < tau_i) {
-                w[k] = 0.0;
-                present[k] = 0;
-            } else {
-                w[k] = wk;
-                lc.push_back({k, wk});
-                for (int32_t q = d0 + 1; q < F->U.rp[k + 1]; ++q) {
-                    int32_t j = F->U.ci[q];
-                    if (!present[j]) {
-                        present[j] = 1;
-                        touched.push_back(j);
-                        if (j < i) bits[j >> 6] |= 1ull << (j & 63);
-                        else if (j > i) upos.push_back(j);
-                    }
-                    w[j] = w[j] - wk * F->U.v[q];
-                }
-            }
-            ++k;
-        }
-        const double diag = present[i] ? w[i] : 0.0;
-        if (diag == 0.0) {
-            if (err_row) *err_row = i;
-            return nullptr;
-        }
-        uc.clear();
-        for (int32_t j : upos)
-            if (!(std::fabs(w[j]) < tau_i)) uc.push_back({j, w[j]});
-        keep_largest(lc, M);
-        keep_largest(uc, M);
-        for (auto& e : lc) { F->L.ci.push_back(e.c); F->L.v.push_back(e.v); }
-        F->L.rp[i + 1] = int32_t(F->L.ci.size());
-        F->U.ci.push_back(i);
-        F->U.v.push_back(diag);
-        for (auto& e : uc) { F->U.ci.push_back(e.c); F->U.v.push_back(e.v); }
-        F->U.rp[i + 1] = int32_t(F->U.ci.size());
-        for (int32_t c : touched) { w[c] = 0.0; present[c] = 0; }
+        F->L.rp[i + 1] = F->L.rp[i] + int32_t(Lr[i].c.size());
+        F->U.rp[i + 1] = F->U.rp[i] + int32_t(Ur[i].c.size());
+    }
+    F->L.ci.reserve(F->L.rp[n]);
+    F->L.v.reserve(F->L.rp[n]);
+    F->U.ci.reserve(F->U.rp[n]);
+    F->U.v.reserve(F->U.rp[n]);
+    for (int32_t i = 0; i < n; ++i) {
+        F->L.ci.insert(F->L.ci.end(), Lr[i].c.begin(), Lr[i].c.end());
+        F->L.v.insert(F->L.v.end(), Lr[i].v.begin(), Lr[i].v.end());
+        std::vector<int32_t>().swap(Lr[i].c);
+        std::vector<double>().swap(Lr[i].v);
+        F->U.ci.insert(F->U.ci.end(), Ur[i].c.begin(), Ur[i].c.end());
+        F->U.v.insert(F->U.v.end(), Ur[i].v.begin(), Ur[i].v.end());
+        std::vector<int32_t>().swap(Ur[i].c);
+        std::vector<double>().swap(Ur[i].v);
     }
     F->levels();
     return F;
@@ -387,13 +477,19 @@ struct Hier {
 };
 
 static void prolong_add(const Csr& P, const double* ML, const double* vc, double* u) {
-    for (int32_t i = 0; i < P.n; ++i) u[i] = u[i] + row_dot(P.rp.data(), P.ci.data(), P.v.data(), i, vc) / ML[i];
+    par_rows(P.n, [&](int32_t i0, int32_t i1) {
+        for (int32_t i = i0; i < i1; ++i) u[i] = u[i] + row_dot(P.rp.data(), P.ci.data(), P.v.data(), i, vc) / ML[i];
+    });
 }
 static void restrict_(const Csr& PT, const double* MLc, const double* rf, double* rc) {
-    for (int32_t j = 0; j < PT.n; ++j) rc[j] = row_dot(PT.rp.data(), PT.ci.data(), PT.v.data(), j, rf) / MLc[j];
+    par_rows(PT.n, [&](int32_t j0, int32_t j1) {
+        for (int32_t j = j0; j < j1; ++j) rc[j] = row_dot(PT.rp.data(), PT.ci.data(), PT.v.data(), j, rf) / MLc[j];
+    });
 }
 static void hprolong_add(const Csr& P, const double* ec, double* e) {
-    for (int32_t i = 0; i < P.n; ++i) e[i] = e[i] + row_dot(P.rp.data(), P.ci.data(), P.v.data(), i, ec);
+    par_rows(P.n, [&](int32_t i0, int32_t i1) {
+        for (int32_t i = i0; i < i1; ++i) e[i] = e[i] + row_dot(P.rp.data(), P.ci.data(), P.v.data(), i, ec);
+    });
 }
 
 // ILUT smoothing step u <- u + U^{-1} L^{-1} (f - A u); `r` may be a
@@ -475,6 +571,8 @@ struct orc_hier_s {
 };
 
 extern "C" {
+
+void orc_set_threads(int n) { g_threads = n < 1 ? 1 : n; }
 
 int orc_spmv(const pmg_csr_view* A, const double* x, double* y) {
     for (int32_t i = 0; i < A->nrows; ++i) y[i] = row_dot(A->rowptr, A->col, A->val, i, x);

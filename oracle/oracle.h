@@ -34,6 +34,8 @@ extern "C" {
 typedef struct orc_factor_s* orc_factor;
 typedef struct orc_hier_s* orc_hier;
 
+/* host threads for the row-independent loops and the ILUT rows (results are identical) */
+void orc_set_threads(int n);
 int orc_spmv(const pmg_csr_view* A, const double* x, double* y);
 int orc_residual(const pmg_csr_view* A, const double* x, const double* f, double* r);
 double orc_norm2(const double* r, int64_t n); /* canonical blocked order */

@@ -43,6 +43,7 @@ def lib():
             subprocess.run(["make", "-C", HERE], check=True, capture_output=True)
         L = ctypes.CDLL(LIB)
         vp, i32, i64, dbl = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
+        L.orc_set_threads.argtypes = [ctypes.c_int]
         L.orc_norm2.restype = dbl
         L.orc_norm2.argtypes = [vp, i64]
         for fn in ("orc_spmv",):
@@ -83,6 +84,11 @@ class OracleError(RuntimeError):
     def __init__(self, status, row=-1, level=-1):
         super().__init__(f"oracle status {status} row {row} level {level}")
         self.status, self.row, self.level = status, row, level
+
+
+def set_threads(n: int) -> None:
+    """Host threads for the oracle's row-independent loops and ILUT rows (results unchanged)."""
+    lib().orc_set_threads(int(n))
 
 
 def spmv(A, x):
@@ -213,6 +219,8 @@ class Hierarchy:
                  factors=None):
         self.desc, self._keep = make_desc(problem, smoother, nu1, nu2, tau, fillfactor, ordering)
         self.n = problem.n
+        self._sizes = ([l.A.nrows for l in problem.plevels[:-1]] if smoother == ILUT else []) + \
+                      [h.A.nrows for h in problem.hlevels[:-1]]
         h = ctypes.c_void_p()
         lvl, row = ctypes.c_int(-1), ctypes.c_int64(-1)
         ext = None
@@ -234,6 +242,7 @@ class Hierarchy:
         out = []
         for k in range(lib().orc_hier_num_factors(self.h)):
             f = Factor(lib().orc_hier_factor(self.h, k), owner=self)
+            f.n = self._sizes[k]
             out.append(f)
         return out
 

@@ -276,6 +276,45 @@ int iga_problem_vec_copy(const iga_problem* h, int kind, int l, double* out) {
     return 0;
 }
 
+// Single operator on one space: kind 0 = CDR operator A (rhs f = 0,
+// optional load in vec F), 1 = mass M, 2 = transfer P^{p}_{p2}, 3 = lumped mass (vec ML).
+int iga_matrix_build(int kind, int geometry, int p, int p2, int nel, const double* D, const double* v, double R,
+                     double nitsche_scale, iga_problem** out) {
+    try {
+        Domain dom = make_domain(geometry);
+        Space sp = Space::build(dom, p, nel);
+        auto* h = new iga_problem_s;
+        h->pb.plev.resize(1);
+        PLevel& L = h->pb.plev[0];
+        L.degree = p;
+        if (kind == 0) {
+            double Dd[4] = {1, 0, 0, 1}, vv[2] = {0, 0};
+            if (D) std::memcpy(Dd, D, sizeof(Dd));
+            if (v) std::memcpy(vv, v, sizeof(vv));
+            Cdr c = make_coeffs(IGA_RHS_ONE, Dd, vv, R);
+            c.nitsche_scale = nitsche_scale > 0 ? nitsche_scale : 1.0;
+            L.A = assemble_operator(dom, sp, c, &h->pb.f);
+        } else if (kind == 1) {
+            L.A = assemble_mass(dom, sp);
+        } else if (kind == 2) {
+            L.A = assemble_transfer(dom, sp, Space::build(dom, p2, nel));
+        } else if (kind == 3) {
+            L.A = assemble_mass(dom, sp);
+            L.ML = lump(L.A);
+        } else {
+            delete h;
+            g_err = "unknown matrix kind";
+            return -1;
+        }
+        *out = h;
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        *out = nullptr;
+        return -1;
+    }
+}
+
 // ---- small entry points mirroring SPEC ops, used by the property tests ----
 int iga_eval_basis(int p, int spans, double x, int with_deriv, double* N, double* dN) {
     try {

@@ -50,6 +50,9 @@ def _host():
         lib.iga_geometry_map.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_double,
                                          ctypes.c_void_p, ctypes.c_void_p]
         lib.iga_set_num_threads.argtypes = [ctypes.c_int]
+        lib.iga_matrix_build.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double, ctypes.c_double,
+                                         ctypes.POINTER(ctypes.c_void_p)]
         lib._typed = True
     return lib
 
@@ -180,6 +183,27 @@ def build(spec: ProblemSpec | int, degree: int = 0, name: str | None = None) -> 
     sd = {k: (list(getattr(spec, k)) if k in ("D", "v", "degrees") else getattr(spec, k)) for k, _ in spec._fields_}
     sd["degrees"] = sd["degrees"][: spec.n_degrees]
     return Problem(name or "custom", sd, pl, hl, f, u0)
+
+
+def matrix(kind: str, geometry: str = "square", p: int = 1, nel: int = 1, p2: int = 1, D=(1, 0, 0, 1), v=(0, 0),
+           R: float = 0.0, nitsche_scale: float = 0.0):
+    """One assembled operator: kind in {"A", "M", "P", "ML"}.
+    Returns a Csr (and, for "A", the load vector f = (1, v); for "ML", the lumped mass)."""
+    lib = _host()
+    k = {"A": 0, "M": 1, "P": 2, "ML": 3}[kind]
+    Dv = np.ascontiguousarray(D, np.float64)
+    vv = np.ascontiguousarray(v, np.float64)
+    h = ctypes.c_void_p()
+    _check(lib.iga_matrix_build(k, GEOM[geometry], p, p2, nel, ptr(Dv), ptr(vv), R, nitsche_scale, ctypes.byref(h)))
+    try:
+        M = _csr(lib, h, MAT_A, 0)
+        if kind == "A":
+            return M, _vec(lib, h, VEC_F, 0)
+        if kind == "ML":
+            return M, _vec(lib, h, VEC_ML, 0)
+        return M
+    finally:
+        lib.iga_problem_free(h)
 
 
 def eval_basis(p: int, spans: int, x: float, deriv: bool = False):
