@@ -335,14 +335,11 @@ class PmgHierarchy:
         np_ = len(self.degrees)
         ids = ([l for l in range(np_ - 1)] if self.smoother == "ilut" else []) + \
               [np_ - 1 + j for j in range(self.nfactors - (np_ - 1 if self.smoother == "ilut" else 0))]
-        for k in ids:
+        for pos, k in enumerate(ids):
             h = ctypes.c_void_p()
             _raise(lib().pmg_hier_factor(self.h, k, ctypes.byref(h)), what="hier_factor")
-            out.append(IlutFactorization(h.value, self._factor_n(k), None, None, owner=self))
+            out.append(IlutFactorization(h.value, self._sizes[pos], None, None, owner=self))
         return out
-
-    def _factor_n(self, k):
-        return self._sizes[k] if hasattr(self, "_sizes") else None
 
     def kernel_times(self, enable=None):
         """Per-class device ms: resid(A_p), L(p), U(p), GS(p), transfers, coarse, misc."""
