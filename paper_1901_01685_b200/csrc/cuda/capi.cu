@@ -3,6 +3,8 @@
 // solve runs in the kernels of sell.cu / trsv.cu / dense.cu; the host only sequences
 // launches on the work stream.
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -13,6 +15,7 @@
 #include "dense.cuh"
 #include "ilut.cuh"
 #include "rcm.hpp"
+#include "skew.cuh"
 #include "sell.cuh"
 #include "trsv.cuh"
 
@@ -81,10 +84,11 @@ DevCsr upload(const pmg_csr_view& v, cudaStream_t st) {
     return d;
 }
 
-bool force_levelsched() {
-    const char* e = getenv("PMG_FORCE_LEVELSCHED");
+bool env_flag(const char* name) {
+    const char* e = getenv(name);
     return e && e[0] == '1';
 }
+bool force_levelsched() { return env_flag("PMG_FORCE_LEVELSCHED"); }
 
 struct Stream {
     cudaStream_t s = nullptr;
@@ -112,6 +116,7 @@ struct pmg_csr_s {
     int32_t* gs_nlow = nullptr;
     int32_t seg = 0;              // chained-segment length (0: level-scheduled sweeps)
     int32_t* gs_split = nullptr;
+    int32_t gs_gap = 0;
     ~pmg_csr_s() {
         A.free();
         sell_free(S);
@@ -138,6 +143,10 @@ struct pmg_factor_s {
     int32_t seg = 0;                  // chained-segment length (0: level-scheduled sweeps)
     int32_t* rev = nullptr;           // v -> row for the U sweep (descending rows)
     int32_t *splitL = nullptr, *splitU = nullptr;
+    bool skew = false;                // skewed-warp sweeps (short rows, short reach)
+    int32_t bs = 32;                  // chain finisher batch
+    int32_t gapL = 0, gapU = 0;       // chain start gates
+    SkewPlan planL, planU;
     ~pmg_factor_s() {
         L.free();
         U.free();
@@ -157,10 +166,15 @@ namespace {
 
 // e = U^{-1} L^{-1} r[perm] added into u[perm]  (y, x: scratch)
 void apply_factor(pmg_factor_s* F, const double* r, double* y, double* x, double* u, int* ticket, cudaStream_t st) {
-    if (F->seg > 0) {
-        ChainOp l{kChainL, &F->Ls, nullptr, nullptr, F->splitL, F->perm, r, nullptr, y, nullptr, F->seg};
+    if (F->skew) {
+        SkewOp l{kSkewL, &F->Ls, nullptr, F->perm, r, y, nullptr, F->seg, F->planL.D};
+        skew_sweep(l, ticket, st);
+        SkewOp up{kSkewU, &F->Us, F->Udiag, F->perm, y, x, u, F->seg, F->planU.D};
+        skew_sweep(up, ticket, st);
+    } else if (F->seg > 0) {
+        ChainOp l{kChainL, &F->Ls, nullptr, nullptr, F->splitL, F->perm, r, nullptr, y, nullptr, F->seg, F->bs, F->gapL};
         chain_sweep(l, ticket, st);
-        ChainOp up{kChainU, &F->Us, F->Udiag, nullptr, F->splitU, F->perm, y, nullptr, x, u, F->seg};
+        ChainOp up{kChainU, &F->Us, F->Udiag, nullptr, F->splitU, F->perm, y, nullptr, x, u, F->seg, F->bs, F->gapU};
         chain_sweep(up, ticket, st);
     } else {
         lsolve(F->Ls, F->perm, r, y, ticket, st);
@@ -170,7 +184,7 @@ void apply_factor(pmg_factor_s* F, const double* r, double* y, double* x, double
 
 void gs_apply(pmg_csr_s* A, const double* f, const double* uo, double* un, int* ticket, cudaStream_t st) {
     if (A->seg > 0) {
-        ChainOp g{kChainGS, &A->gs, A->gs_diag, A->gs_nlow, A->gs_split, nullptr, f, uo, un, nullptr, A->seg};
+        ChainOp g{kChainGS, &A->gs, A->gs_diag, A->gs_nlow, A->gs_split, nullptr, f, uo, un, nullptr, A->seg, 8, A->gs_gap};
         chain_sweep(g, ticket, st);
     } else {
         gs_sweep(A->gs, A->gs_diag, A->gs_nlow, f, uo, un, ticket, st);
@@ -201,6 +215,7 @@ void ensure_gs(pmg_csr_s* h, cudaStream_t st) {
     if (h->seg > 0) {
         h->gs_split = dalloc<int32_t>(n);
         chain_split(h->gs, h->gs_nlow, h->seg, kChainGS, h->gs_split, st);
+        h->gs_gap = chain_start_gap(h->gs, h->gs_split, h->seg, kChainGS, st);
     }
     // first row (in row order) with a zero or missing diagonal -> SPEC.md:237 smoother error
     std::vector<double> dg(n);
@@ -263,6 +278,10 @@ int make_factor(pmg_csr_s* A, double tau, double fillfactor, int ordering, pmg_f
         F->splitU = dalloc<int32_t>(n);
         chain_split(F->Ls, nullptr, F->seg, kChainL, F->splitL, st);
         chain_split(F->Us, nullptr, F->seg, kChainU, F->splitU, st);
+        F->gapL = chain_start_gap(F->Ls, F->splitL, F->seg, kChainL, st);
+        F->gapU = chain_start_gap(F->Us, F->splitU, F->seg, kChainU, st);
+        if (getenv("PMG_VERBOSE"))
+            fprintf(stderr, "[pmg] factor n=%d seg=%d bs=%d gapL=%d gapU=%d\n", F->n, F->seg, F->bs, F->gapL, F->gapU);
     } else {
         sell_build(F->Ls, n, F->L.rowptr, F->L.col, F->L.val, F->lvL.order, kPickAll, nullptr, nullptr, st);
         sell_build(F->Us, n, F->U.rowptr, F->U.col, F->U.val, F->lvU.order, kPickOffDiagDesc, F->Udiag, nullptr, st);
@@ -276,6 +295,14 @@ int make_factor(pmg_csr_s* A, double tau, double fillfactor, int ordering, pmg_f
     for (int32_t i = 0; i < n; ++i) {
         F->max_row_L = std::max(F->max_row_L, lr[i + 1] - lr[i]);
         F->max_row_U = std::max(F->max_row_U, ur[i + 1] - ur[i]);
+    }
+    // short rows (p=1 factors): the per-segment lag is dominated by the finisher batch
+    F->bs = std::max(F->max_row_L, F->max_row_U) <= 16 ? 8 : 32;
+    if (const char* e = getenv("PMG_CHAIN_BS")) F->bs = atoi(e);
+    if (F->seg > 0 && env_flag("PMG_SKEW")) {  // experimental, off by default
+        const bool okL = skew_plan(F->Ls, F->seg, kSkewL, F->max_row_L, F->planL, st);
+        const bool okU = skew_plan(F->Us, F->seg, kSkewU, F->max_row_U - 1, F->planU, st);
+        F->skew = okL && okU;
     }
     *out = F.release();
     return PMG_OK;
@@ -436,13 +463,22 @@ void smooth_ilut(pmg_work_s& W, pmg_csr_s* A, pmg_factor_s* F, double* u, const 
         W.run(fine ? kClsResid0 : kClsCoarse, 1, [&] { sell_rowop(A->S, kOpResidual, u, f, nullptr, r, nullptr, W.st); });
         rr = r;
     }
-    if (F->seg > 0) {
+    if (F->skew) {
+        W.run(fine ? kClsL0 : kClsCoarse, 4, [&] {
+            SkewOp l{kSkewL, &F->Ls, nullptr, F->perm, rr, y, nullptr, F->seg, F->planL.D};
+            skew_sweep(l, W.ticket, W.st);
+        });
+        W.run(fine ? kClsU0 : kClsCoarse, 4, [&] {
+            SkewOp up{kSkewU, &F->Us, F->Udiag, F->perm, y, x, u, F->seg, F->planU.D};
+            skew_sweep(up, W.ticket, W.st);
+        });
+    } else if (F->seg > 0) {
         W.run(fine ? kClsL0 : kClsCoarse, 3, [&] {
-            ChainOp l{kChainL, &F->Ls, nullptr, nullptr, F->splitL, F->perm, rr, nullptr, y, nullptr, F->seg};
+            ChainOp l{kChainL, &F->Ls, nullptr, nullptr, F->splitL, F->perm, rr, nullptr, y, nullptr, F->seg, F->bs, F->gapL};
             chain_sweep(l, W.ticket, W.st);
         });
         W.run(fine ? kClsU0 : kClsCoarse, 3, [&] {
-            ChainOp up{kChainU, &F->Us, F->Udiag, nullptr, F->splitU, F->perm, y, nullptr, x, u, F->seg};
+            ChainOp up{kChainU, &F->Us, F->Udiag, nullptr, F->splitU, F->perm, y, nullptr, x, u, F->seg, F->bs, F->gapU};
             chain_sweep(up, W.ticket, W.st);
         });
     } else {

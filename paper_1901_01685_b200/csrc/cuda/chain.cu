@@ -54,6 +54,9 @@ struct ChainArgs {
     int* ticket;
     int* prog;      // [nseg] rows finalised per segment (throttling hint, relaxed)
     int ahead;      // helper lookahead (rows beyond the finisher)
+    int bs;         // finisher batch (rows per broadcast round, <= 32)
+    int stager_async;  // 1: cp.async staging; 0: plain loads + shared stores
+    int gate_all;      // 1: whole CTA waits for the start gate; 0: only the finisher
     int start_gap;  // a segment starts once its predecessor finalised this many rows
     unsigned long long* trace;  // optional: per segment [claim, helpers done, fin start, fin end, hspins, fwaits]
 };
@@ -125,7 +128,7 @@ __global__ void __launch_bounds__(NT) k_chain(ChainArgs a) {
             if (a.trace) a.trace[sg * 6 + 0] = gtimer();
             // idle until the predecessor is under way: segments far ahead of the wavefront
             // would only thrash L2 with work that waits anyway
-            if (sg > 0) {
+            if (sg > 0 && a.gate_all) {
                 const int need = min(a.start_gap, a.seg);
                 unsigned ns = 64;
                 while (*reinterpret_cast<volatile int*>(a.prog + sg - 1) < need) {
@@ -243,10 +246,31 @@ __global__ void __launch_bounds__(NT) k_chain(ChainArgs a) {
                     const int* cb = a.S.col + base + (v & 31) * 4;
                     const double* vb = a.S.val + base + (v & 31) * 2;
                     wait_fin(&sm.fin_done, v - RS);
-                    for (int q = 0; q < m; ++q) {
-                        const int kk = f0 + q;
-                        cp_async4(&sm.ecol[q][es], cb + (kk >> 2) * 128 + (kk & 3));
-                        cp_async8(&sm.eval_[q][es], vb + (kk >> 1) * 64 + (kk & 1));
+                    if (a.stager_async) {
+                        for (int q = 0; q < m; ++q) {
+                            const int kk = f0 + q;
+                            cp_async4(&sm.ecol[q][es], cb + (kk >> 2) * 128 + (kk & 3));
+                            cp_async8(&sm.eval_[q][es], vb + (kk >> 1) * 64 + (kk & 1));
+                        }
+                    } else {
+                        for (int q0 = 0; q0 < m; q0 += 8) {  // 8 loads in flight, then 8 stores
+                            int c[8];
+                            double w[8];
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) {
+                                const int kk = f0 + q0 + q;
+                                if (q0 + q < m) {
+                                    c[q] = __ldg(cb + (kk >> 2) * 128 + (kk & 3));
+                                    w[q] = __ldg(vb + (kk >> 1) * 64 + (kk & 1));
+                                }
+                            }
+#pragma unroll
+                            for (int q = 0; q < 8; ++q)
+                                if (q0 + q < m) {
+                                    sm.ecol[q0 + q][es] = c[q];
+                                    sm.eval_[q0 + q][es] = w[q];
+                                }
+                        }
                     }
                 }
                 cp_async_commit();
@@ -274,12 +298,22 @@ __global__ void __launch_bounds__(NT) k_chain(ChainArgs a) {
             // ------------------------------------------------------------ finisher
             // batches of 32 rows; lane k owns row lo + 32b + k of batch b.  Only shared memory
             // and registers on the hot path.
+            if (sg > 0 && !a.gate_all && lane == 0) {  // helpers/stager already run; gate the finisher
+                const int need = min(a.start_gap, a.seg);
+                unsigned ns = 32;
+                while (*reinterpret_cast<volatile int*>(a.prog + sg - 1) < need) {
+                    __nanosleep(ns);
+                    ns = min(ns * 2, 256u);
+                }
+            }
+            __syncwarp();
             if (a.trace && lane == 0) a.trace[sg * 6 + 2] = gtimer();
-            const int nb = (hi - lo + 31) >> 5;
+            const int bs = a.bs;
+            const int nb = (hi - lo + bs - 1) / bs;
             for (int b = 0; b < nb; ++b) {
-                const int t0 = lo + 32 * b;
+                const int t0 = lo + bs * b;
                 const int v = t0 + lane;
-                const bool live = v < hi;
+                const bool live = lane < bs && v < hi;
                 unsigned long long* bt =
                     (a.trace && sg == 8 && b < 64 && lane == 0) ? a.trace + a.nseg * 6 + b * 5 : nullptr;
                 if (bt) bt[0] = gtimer();
@@ -325,7 +359,7 @@ __global__ void __launch_bounds__(NT) k_chain(ChainArgs a) {
                     if (pos < cnt) entry(pos, nc, nv);
                 }
                 if (bt) bt[3] = gtimer();
-                const int tend = min(hi, t0 + 32);
+                const int tend = min(hi, t0 + bs);
                 for (int t = t0; t < tend; ++t) {
                     const int f = t - t0;
                     double y = 0.0;
@@ -364,6 +398,22 @@ __global__ void __launch_bounds__(NT) k_chain(ChainArgs a) {
 }  // namespace
 
 namespace {
+// forward reach into the previous segment: max over rows of (jx - ix + 1); a segment's first
+// batch of bs rows needs reach + bs finalised rows of its predecessor (the start gate)
+__global__ void k_chain_gap(Sell S, const int32_t* __restrict__ split, int32_t seg, int K, int* out) {
+    const int32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= S.n) return;
+    const int n = S.n, g = v / seg;
+    const int64_t base = S.off[v >> 5];
+    const int li = v & 31;
+    int need = 0;
+    for (int k = 0; k < split[v]; ++k) {
+        int c = S.col[base + (k >> 2) * 128 + li * 4 + (k & 3)];
+        if (K == kChainU) c = n - 1 - c;
+        if (c / seg == g - 1) need = max(need, c - (g - 1) * seg - (v - g * seg) + 1);
+    }
+    atomicMax(out, need);
+}
 __global__ void k_chain_split(Sell S, const int32_t* __restrict__ nlow, int32_t seg, int K, int32_t* __restrict__ split) {
     const int32_t v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= S.n) return;
@@ -387,6 +437,20 @@ bool g_chain_trace_on = false;
 unsigned long long* g_chain_trace = nullptr;
 size_t g_chain_trace_cap = 0;
 int g_chain_trace_n = 0;
+
+int32_t chain_start_gap(const Sell& S, const int32_t* split, int32_t seg, ChainKind kind, cudaStream_t st) {
+    if (S.n == 0 || seg <= 0) return 1;
+    int* d;
+    PMG_CUDA(cudaMallocAsync(&d, sizeof(int), st));
+    PMG_CUDA(cudaMemsetAsync(d, 0, sizeof(int), st));
+    k_chain_gap<<<ceil_div(S.n, 256), 256, 0, st>>>(S, split, seg, int(kind), d);
+    PMG_LAUNCH_CHECK();
+    int h = 0;
+    PMG_CUDA(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, st));
+    PMG_CUDA(cudaStreamSynchronize(st));
+    PMG_CUDA(cudaFreeAsync(d, st));
+    return std::max(h, 1);
+}
 
 void chain_split(const Sell& S, const int32_t* nlow, int32_t seg, ChainKind kind, int32_t* split, cudaStream_t st) {
     if (S.n == 0) return;
@@ -412,11 +476,47 @@ void chain_sweep(const ChainOp& op, int* ticket, cudaStream_t st) {
     if (ahead < 0) {
         const char* e = getenv("PMG_CHAIN_AHEAD");
         ahead = e ? atoi(e) : 96;
-        const char* g = getenv("PMG_CHAIN_START_GAP");
-        gap = g ? atoi(g) : 48;
+        const char* g = getenv("PMG_CHAIN_START_GAP");  // forces the gate (tuning)
+        gap = g ? atoi(g) : 0;
     }
-    ChainArgs a{*op.S, op.diag, op.nlow, op.split, op.perm, op.rhs, op.old, op.out, op.upd, n, op.seg,
-                nseg, ticket, prog, ahead, gap, nullptr};
+    ChainArgs a{};
+    a.S = *op.S;
+    a.diag = op.diag;
+    a.nlow = op.nlow;
+    a.split = op.split;
+    a.perm = op.perm;
+    a.rhs = op.rhs;
+    a.old = op.old;
+    a.out = op.out;
+    a.upd = op.upd;
+    a.n = n;
+    a.seg = op.seg;
+    a.nseg = nseg;
+    a.ticket = ticket;
+    a.prog = prog;
+    a.ahead = ahead;
+    a.bs = op.bs > 0 && op.bs <= 32 ? op.bs : 32;
+    static int cap = -1;
+    if (cap < 0) {
+        const char* e = getenv("PMG_CHAIN_GAP_CAP");
+        cap = e ? atoi(e) : 48;
+    }
+    // a gate at the data reach would let each segment start only when its first row can
+    // finish, exposing the start-up latency; capping it starts long-reach segments early
+    a.start_gap = gap > 0 ? gap : op.start_gap > 0 ? std::min(op.start_gap, cap) : cap;
+    static int stager_async = -1;
+    if (stager_async < 0) {
+        const char* e = getenv("PMG_STAGER_ASYNC");
+        stager_async = e ? atoi(e) : 1;
+    }
+    a.stager_async = stager_async;
+    static int gate_all = -1;
+    if (gate_all < 0) {
+        const char* e = getenv("PMG_GATE_ALL");
+        gate_all = e ? atoi(e) : 1;
+    }
+    a.gate_all = gate_all;
+    a.trace = nullptr;
     if (g_chain_trace_on) {
         const size_t need = size_t(a.nseg) * 6 + 64 * 5 + 1024;
         if (need > g_chain_trace_cap) {

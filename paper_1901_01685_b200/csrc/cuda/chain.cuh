@@ -19,7 +19,12 @@ struct ChainOp {
     double* out;               // v-space outputs with sentinel protocol (L: y, U: x_v, GS: u_new)
     double* upd;               // U: u
     int32_t seg;               // segment length (rows)
+    int32_t bs = 32;           // finisher batch: smaller for short-reach factors (lag ~ bs + reach)
+    int32_t start_gap = 0;     // rows of the predecessor segment needed before a segment starts (0: default)
 };
+
+// data-driven start gate: max over rows of the last previous-segment row they reference, + 1
+int32_t chain_start_gap(const Sell& S, const int32_t* split, int32_t seg, ChainKind kind, cudaStream_t st);
 
 // per-row split point between earlier-segment entries and in-segment entries
 void chain_split(const Sell& S, const int32_t* nlow, int32_t seg, ChainKind kind, int32_t* split, cudaStream_t st);

@@ -1,5 +1,7 @@
 cd $GRAFT_REPO_ROOT
-for cfg in "64 64" "48 64" "32 64" "64 32" "80 48"; do
-  set -- $cfg
-  echo "AHEAD=$1 GAP=$2: $(PMG_CHAIN_AHEAD=$1 PMG_CHAIN_START_GAP=$2 timeout 300 python scripts/diag_chain.py 9 5 2>&1 | grep -E 'span' | sed 's/per-seg fin duration median [0-9.]* us;//; s/fin_start lag median [0-9.]* us//' | tr '\n' ' ')"
+for c in 48 32 20; do
+  PMG_CHAIN_GAP_CAP=$c timeout 600 python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/t.json 2> gpurun_out/t.err
+  python -c "
+import json; d=json.load(open('gpurun_out/t.json'))
+print('CAP $c ms/step',round(d['ms_per_step'],1),{k:round(v['ms_total']/max(v['launches'],1),2) for k,v in d['kernel_ms'].items() if v['launches']})"
 done

@@ -1,2 +1,2 @@
 cd $GRAFT_REPO_ROOT
-./scripts/ubench/step_loop2
+./scripts/ubench/step_loop3

@@ -15,14 +15,17 @@ from paper_1901_01685_b200 import problems as P
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["chain", "levelsched"])
+@pytest.fixture(params=["chain", "skew+chain", "levelsched"])
 def sweep_path(request, monkeypatch):
-    """Both sweep implementations must match the oracle: the chained-segment wavefront
-    (default for tensor-grid orderings) and the level-scheduled sync-free fallback."""
+    """Every sweep implementation must match the oracle: the chained-segment wavefront
+    (default for tensor-grid orderings), the experimental skewed-warp kernel for short-row
+    factors (PMG_SKEW=1) and the level-scheduled fallback."""
+    monkeypatch.delenv("PMG_FORCE_LEVELSCHED", raising=False)
+    monkeypatch.delenv("PMG_SKEW", raising=False)
     if request.param == "levelsched":
         monkeypatch.setenv("PMG_FORCE_LEVELSCHED", "1")
-    else:
-        monkeypatch.delenv("PMG_FORCE_LEVELSCHED", raising=False)
+    elif request.param == "skew+chain":
+        monkeypatch.setenv("PMG_SKEW", "1")
     return request.param
 
 RTOL_RHO = 1e-10
