@@ -117,6 +117,7 @@ struct pmg_csr_s {
     int32_t seg = 0;              // chained-segment length (0: level-scheduled sweeps)
     int32_t* gs_split = nullptr;
     int32_t gs_gap = 0;
+    bool gs_chain = false;        // chained GS sweep (else level-scheduled)
     ~pmg_csr_s() {
         A.free();
         sell_free(S);
@@ -183,7 +184,7 @@ void apply_factor(pmg_factor_s* F, const double* r, double* y, double* x, double
 }
 
 void gs_apply(pmg_csr_s* A, const double* f, const double* uo, double* un, int* ticket, cudaStream_t st) {
-    if (A->seg > 0) {
+    if (A->gs_chain) {
         ChainOp g{kChainGS, &A->gs, A->gs_diag, A->gs_nlow, A->gs_split, nullptr, f, uo, un, nullptr, A->seg, 8, A->gs_gap};
         chain_sweep(g, ticket, st);
     } else {
@@ -212,10 +213,20 @@ void ensure_gs(pmg_csr_s* h, cudaStream_t st) {
     h->gs_nlow = dalloc<int32_t>(n);
     sell_build(h->gs, n, h->A.rowptr, h->A.col, h->A.val, h->seg > 0 ? nullptr : h->gs_lv.order, kPickOffDiag,
                h->gs_diag, h->gs_nlow, st);
-    if (h->seg > 0) {
+    h->gs_chain = h->seg > 0;
+    if (h->gs_chain) {
         h->gs_split = dalloc<int32_t>(n);
         chain_split(h->gs, h->gs_nlow, h->seg, kChainGS, h->gs_split, st);
-        h->gs_gap = chain_start_gap(h->gs, h->gs_split, h->seg, kChainGS, st);
+        const ChainPlan pl = chain_plan(h->gs, h->gs_nlow, h->gs_split, h->seg, kChainGS, st);
+        h->gs_gap = pl.gap;
+        if (!pl.ok) {  // rows exceed the chain kernel's on-chip buffers: level-scheduled sweep
+            h->gs_chain = false;
+            sell_free(h->gs);
+            cudaFree(h->gs_split);
+            h->gs_split = nullptr;
+            sell_build(h->gs, n, h->A.rowptr, h->A.col, h->A.val, h->gs_lv.order, kPickOffDiag, h->gs_diag,
+                       h->gs_nlow, st);
+        }
     }
     // first row (in row order) with a zero or missing diagonal -> SPEC.md:237 smoother error
     std::vector<double> dg(n);
@@ -225,7 +236,7 @@ void ensure_gs(pmg_csr_s* h, cudaStream_t st) {
     PMG_CUDA(cudaStreamSynchronize(st));
     int64_t zr = -1;
     for (int32_t p = 0; p < n; ++p) {
-        const int32_t row = h->seg > 0 ? p : ord[p];
+        const int32_t row = h->gs_chain ? p : ord[p];
         if (dg[p] == 0.0 && (zr < 0 || row < zr)) zr = row;
     }
     h->gs_zero_row = zr;
@@ -267,7 +278,8 @@ int make_factor(pmg_csr_s* A, double tau, double fillfactor, int ordering, pmg_f
     level_sets(F->lvL, n, F->L.rowptr, F->L.col, kDepLower, st);
     level_sets(F->lvU, n, F->U.rowptr, F->U.col, kDepUpper, st);
     F->Udiag = dalloc<double>(n);
-    if (F->seg > 0) {  // chained-segment layouts: L in row order, U in descending row order
+    bool chain = F->seg > 0;
+    if (chain) {  // chained-segment layouts: L in row order, U in descending row order
         F->rev = dalloc<int32_t>(n);
         std::vector<int32_t> rv(n);
         for (int32_t v = 0; v < n; ++v) rv[v] = n - 1 - v;
@@ -278,11 +290,25 @@ int make_factor(pmg_csr_s* A, double tau, double fillfactor, int ordering, pmg_f
         F->splitU = dalloc<int32_t>(n);
         chain_split(F->Ls, nullptr, F->seg, kChainL, F->splitL, st);
         chain_split(F->Us, nullptr, F->seg, kChainU, F->splitU, st);
-        F->gapL = chain_start_gap(F->Ls, F->splitL, F->seg, kChainL, st);
-        F->gapU = chain_start_gap(F->Us, F->splitU, F->seg, kChainU, st);
+        const ChainPlan pl = chain_plan(F->Ls, nullptr, F->splitL, F->seg, kChainL, st);
+        const ChainPlan pu = chain_plan(F->Us, nullptr, F->splitU, F->seg, kChainU, st);
+        F->gapL = pl.gap;
+        F->gapU = pu.gap;
         if (getenv("PMG_VERBOSE"))
-            fprintf(stderr, "[pmg] factor n=%d seg=%d bs=%d gapL=%d gapU=%d\n", F->n, F->seg, F->bs, F->gapL, F->gapU);
-    } else {
+            fprintf(stderr, "[pmg] factor n=%d seg=%d gap %d/%d in-seg %d/%d back %d/%d\n", F->n, F->seg, pl.gap,
+                    pu.gap, pl.max_in, pu.max_in, pl.max_back, pu.max_back);
+        if (!(pl.ok && pu.ok)) {  // rows exceed the chain kernel's on-chip buffers: level-scheduled sweeps
+            chain = false;
+            F->seg = 0;
+            sell_free(F->Ls);
+            sell_free(F->Us);
+            cudaFree(F->rev);
+            cudaFree(F->splitL);
+            cudaFree(F->splitU);
+            F->rev = F->splitL = F->splitU = nullptr;
+        }
+    }
+    if (!chain) {
         sell_build(F->Ls, n, F->L.rowptr, F->L.col, F->L.val, F->lvL.order, kPickAll, nullptr, nullptr, st);
         sell_build(F->Us, n, F->U.rowptr, F->U.col, F->U.val, F->lvU.order, kPickOffDiagDesc, F->Udiag, nullptr, st);
     }
@@ -1070,7 +1096,7 @@ int pmg_debug_chain_trace(int mode, unsigned long long* out, int cap) {
         return 0;
     }
     if (!g_chain_trace || !out) return 0;
-    const int n = std::min(g_chain_trace_n * 6 + 64 * 5 + 1024, cap);
+    const int n = std::min(g_chain_trace_n * 6 + kChainTraceExtra, cap);
     if (cudaDeviceSynchronize() != cudaSuccess) return -1;
     if (cudaMemcpy(out, g_chain_trace, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
     return g_chain_trace_n;

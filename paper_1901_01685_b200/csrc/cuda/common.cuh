@@ -50,6 +50,13 @@ __device__ __forceinline__ double ld_relaxed_nb(const double* p) {
 __device__ __forceinline__ void st_relaxed(double* p, double v) {
     asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
+// predicated relaxed store without a compiler barrier: publishes one lane's value from
+// branch-free code (consumers poll each element individually, so no ordering is needed)
+__device__ __forceinline__ void st_relaxed_if(double* p, double v, bool pred) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.relaxed.gpu.global.f64 [%0], %1;\n\t}" ::"l"(p),
+        "d"(v), "r"(int(pred)));
+}
 __device__ __forceinline__ int ld_acquire(const int* p) {
     int v;
     asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");

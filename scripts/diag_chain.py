@@ -16,7 +16,7 @@ for lev, A in (('p', pb.plevels[0].A), ('p1', pb.plevels[1].A)):
     e = pmg.ilut_apply(F, r)
     L.pmg_debug_chain_trace(1, None, 0)
     t = time.time(); e = pmg.ilut_apply(F, r); ta = time.time() - t
-    buf = np.zeros(6 * 5000 + 64 * 5 + 1024, np.uint64)
+    buf = np.zeros(6 * 5000 + 640 + 4096 + 32, np.uint64)
     nseg = L.pmg_debug_chain_trace(-1, buf.ctypes.data_as(ctypes.c_void_p), buf.size)
     L.pmg_debug_chain_trace(0, None, 0)
     tr = buf[:6 * nseg].reshape(nseg, 6).astype(np.float64)
@@ -27,17 +27,34 @@ for lev, A in (('p', pb.plevels[0].A), ('p1', pb.plevels[1].A)):
           f"lag(fin_end) median {np.median(np.diff(fe)):.2f} us; fin_start lag median {np.median(np.diff(fs)):.2f} us")
     print(f"  helper spins median {np.median(tr[:,4]):.0f} fin batch waits median {np.median(tr[:,5]):.0f}; "
           f"helpers done - fin start median {np.median(hdone-fs):.1f} us")
-    bt = buf[6 * nseg: 6 * nseg + 64 * 5].reshape(64, 5).astype(np.float64)
-    hp = buf[6 * nseg + 64 * 5: 6 * nseg + 64 * 5 + 1024].astype(np.float64)
+    ex = buf[6 * nseg: 6 * nseg + 640].reshape(2, 64, 5).astype(np.float64)
+    hr = buf[6 * nseg + 640: 6 * nseg + 640 + 4096].reshape(2, 1024, 2).astype(np.float64)
     seglen = A.nrows // nseg
-    hp = (hp[:seglen] - t0) / 1e3
-    print("   seg8 helper prefix ready (us) at rows 0,31,63,95,127,191,255,383,511:", [round(hp[i], 1) for i in (0, 31, 63, 95, 127, 191, 255, 383, 511) if i < seglen])
-    print("   seg7 fin_end %.1f, seg8 claim %.1f fin_end %.1f" % (fe[7], claim[8], fe[8]))
-    nb = int((bt[:, 0] > 0).sum())
-    b0 = t0
-    for b in range(min(nb, 6)):
-        print(f"   seg8 batch {b}: start {(bt[b,0]-b0)/1e3:.2f} hdr {(bt[b,1]-bt[b,0])/1e3:.2f} cpwait {(bt[b,2]-bt[b,1])/1e3:.2f} "
-              f"catchup {(bt[b,3]-bt[b,2])/1e3:.2f} steps {(bt[b,4]-bt[b,3])/1e3:.2f} us")
+    cts = buf[6 * nseg + 640 + 4096: 6 * nseg + 640 + 4096 + 32].astype(np.float64)
+    cts = cts[cts > 0]
+    if cts.size:
+        print("  seg8 row160 helper: start %.2f chunk stamps (us from start):" % ((hr[1, 160, 0] - ex[0, 0, 4]) / 1e3),
+              [round((c - hr[1, 160, 0]) / 1e3, 2) for c in cts], "pub %.2f" % ((hr[1, 160, 1] - hr[1, 160, 0]) / 1e3))
+    Lf = F.export()[0]
+    need = np.zeros(min(seglen, 1024), np.int64)  # seg-7 row each seg-8 row needs last
+    for r in range(len(need)):
+        v = 8 * seglen + r
+        cols = Lf.col[Lf.rowptr[v]:Lf.rowptr[v + 1]]
+        c7 = cols[(cols >= 7 * seglen) & (cols < 8 * seglen)] - 7 * seglen
+        need[r] = c7.max() if c7.size else -1
+    bs = 8 if max(F.stats()['max_row_L'], F.stats()['max_row_U']) <= 16 else 32
+    def fin_time(si, row):  # end of the batch of segment 7+si that finalised `row`
+        return ex[si, row // bs, 4]
+    print(f"  bs {bs}; seg8 rows need seg7 row up to max {need.max()}")
+    print("   row | s7 fin(need) | s8 h.start  h.pub | s8 fin | hop(pub - s7fin)  (us, rel. to s7 fin of row 0)")
+    base = ex[0, 0, 4]
+    hops = []
+    for r in list(range(0, 40, 4)) + list(range(64, min(seglen, 1024), 96)):
+        if r >= len(need) or need[r] < 0 or need[r] // bs >= 64 or r // bs >= 64:
+            continue
+        f7 = fin_time(0, need[r]); hs, hp = hr[1, r]; f8 = fin_time(1, r)
+        hops.append(hp - f7)
+        print(f"   {r:4d} | {(f7-base)/1e3:9.2f} | {(hs-base)/1e3:9.2f} {(hp-base)/1e3:9.2f} | {(f8-base)/1e3:8.2f} | {(hp-f7)/1e3:7.2f}")
     for k in list(range(0, 6)) + [nseg // 2, nseg // 2 + 1, nseg - 1]:
         print(f"   seg {k}: claim {claim[k]:.1f} fin_start {fs[k]:.1f} fin_end {fe[k]:.1f} hdone {hdone[k]:.1f} "
               f"spins {tr[k,4]:.0f} waits {tr[k,5]:.0f}")

@@ -1,2 +1,2 @@
 cd $GRAFT_REPO_ROOT
-timeout 600 python scripts/diag_chain.py 9 5 2>&1 | grep -E "^.p|span|seg8 batch|prefix|seg7"
+timeout 600 python scripts/diag_chain.py ${1:-10} ${2:-5} 2>&1 | tail -60
