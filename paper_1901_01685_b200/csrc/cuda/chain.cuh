@@ -43,7 +43,7 @@ void chain_split(const Sell& S, const int32_t* nlow, int32_t seg, ChainKind kind
 // [claim, helpers done, fin start, fin end, helper spins, finisher waits], then for segments
 // 7 and 8: 64 batches x [start, hdr ok, catch-up start, steps start, end], then 1024 rows x
 // [helper row start, prefix published]
-constexpr int kChainTraceExtra = 2 * 64 * 5 + 2 * 2048 + 32;  // + per-chunk stamps of one helper row
+constexpr int kChainTraceExtra = 2 * 64 * 5 + 2 * 2048 + 64;  // + per-chunk stamps of one helper row
 extern bool g_chain_trace_on;
 extern unsigned long long* g_chain_trace;
 extern size_t g_chain_trace_cap;

@@ -77,16 +77,24 @@ __device__ __forceinline__ double wait_value(const double* x, int j) {
 }
 
 // streaming 128-bit loads of matrix data (read once per sweep)
+#ifndef PMG_SELL_LD
+#define PMG_SELL_LD 0
+#endif
+#if PMG_SELL_LD == 0
+#define PMG_SELL_QUAL "ld.global.nc.L1::no_allocate"
+#elif PMG_SELL_LD == 1
+#define PMG_SELL_QUAL "ld.global.cg"
+#else
+#define PMG_SELL_QUAL "ld.global"
+#endif
 __device__ __forceinline__ int4 ld_stream_i4(const int4* p) {
     int4 r;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-                 : "l"(p));
+    asm volatile(PMG_SELL_QUAL ".v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
     return r;
 }
 __device__ __forceinline__ double2 ld_stream_d2(const double2* p) {
     double2 r;
-    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+    asm volatile(PMG_SELL_QUAL ".v2.f64 {%0,%1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
     return r;
 }
 

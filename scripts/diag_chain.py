@@ -16,7 +16,7 @@ for lev, A in (('p', pb.plevels[0].A), ('p1', pb.plevels[1].A)):
     e = pmg.ilut_apply(F, r)
     L.pmg_debug_chain_trace(1, None, 0)
     t = time.time(); e = pmg.ilut_apply(F, r); ta = time.time() - t
-    buf = np.zeros(6 * 5000 + 640 + 4096 + 32, np.uint64)
+    buf = np.zeros(6 * 5000 + 640 + 4096 + 64, np.uint64)
     nseg = L.pmg_debug_chain_trace(-1, buf.ctypes.data_as(ctypes.c_void_p), buf.size)
     L.pmg_debug_chain_trace(0, None, 0)
     tr = buf[:6 * nseg].reshape(nseg, 6).astype(np.float64)
@@ -30,11 +30,13 @@ for lev, A in (('p', pb.plevels[0].A), ('p1', pb.plevels[1].A)):
     ex = buf[6 * nseg: 6 * nseg + 640].reshape(2, 64, 5).astype(np.float64)
     hr = buf[6 * nseg + 640: 6 * nseg + 640 + 4096].reshape(2, 1024, 2).astype(np.float64)
     seglen = A.nrows // nseg
-    cts = buf[6 * nseg + 640 + 4096: 6 * nseg + 640 + 4096 + 32].astype(np.float64)
-    cts = cts[cts > 0]
-    if cts.size:
-        print("  seg8 row160 helper: start %.2f chunk stamps (us from start):" % ((hr[1, 160, 0] - ex[0, 0, 4]) / 1e3),
-              [round((c - hr[1, 160, 0]) / 1e3, 2) for c in cts], "pub %.2f" % ((hr[1, 160, 1] - hr[1, 160, 0]) / 1e3))
+    cts = buf[6 * nseg + 640 + 4096: 6 * nseg + 640 + 4096 + 64].astype(np.float64)
+    h0 = hr[1, 160, 0]
+    if cts[0] > 0:
+        c0 = cts[0]
+        print("  seg8 row160 helper: pub %.2f us after start; per chunk [start, S wait done, y ready] cycles from first chunk:"
+              % ((hr[1, 160, 1] - h0) / 1e3))
+        print("   ", [(int(cts[i] - c0), int(cts[21 + i] - c0), int(cts[42 + i] - c0)) for i in range(21) if cts[i] > 0])
     Lf = F.export()[0]
     need = np.zeros(min(seglen, 1024), np.int64)  # seg-7 row each seg-8 row needs last
     for r in range(len(need)):
@@ -58,3 +60,10 @@ for lev, A in (('p', pb.plevels[0].A), ('p1', pb.plevels[1].A)):
     for k in list(range(0, 6)) + [nseg // 2, nseg // 2 + 1, nseg - 1]:
         print(f"   seg {k}: claim {claim[k]:.1f} fin_start {fs[k]:.1f} fin_end {fe[k]:.1f} hdone {hdone[k]:.1f} "
               f"spins {tr[k,4]:.0f} waits {tr[k,5]:.0f}")
+    if os.environ.get("DIAG_BATCHES"):
+        print("   b | s7 start hdr_ok end | s8 start hdr_ok end | s8 helper row 32b start / row 32b+31 pub")
+        for b in range(min(20, seglen // bs)):
+            r0, r1 = b * bs, b * bs + bs - 1
+            f = lambda x: (x - base) / 1e3
+            print(f"  {b:2d} | {f(ex[0,b,0]):7.2f} {f(ex[0,b,1]):7.2f} {f(ex[0,b,4]):7.2f} | {f(ex[1,b,0]):7.2f} {f(ex[1,b,1]):7.2f} {f(ex[1,b,4]):7.2f} |"
+                  f" {f(hr[1,r0,0]):7.2f} {f(hr[1,r1,1]):7.2f}")
