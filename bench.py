@@ -247,9 +247,17 @@ def main():
     bytes_dom = ab[dom]
     achieved = bytes_dom / (per_launch_ms * 1e-3) / 1e9
     peak, peak_kind = peaks()
+    traffic, traffic_src = ncu_traffic(dom, args)
     roof = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": None, "peak_source": peak_kind, "bytes_per_launch": bytes_dom,
-            "ms_per_launch": per_launch_ms, "launches": launches_dom}
+            "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_kind, "bytes_per_launch": bytes_dom,
+            "ms_per_launch": per_launch_ms, "launches": launches_dom,
+            "note": "triangular sweeps are bounded by their dependency depth (see 'triangular'), not by HBM"}
+    # the HBM-bound kernel of the cycle (residual SpMV), for kernel quality
+    if la.get("resid_fine", 0) > 0:
+        r_ms = ms["resid_fine"] / la["resid_fine"]
+        r_ach = ab["resid_fine"] / (r_ms * 1e-3) / 1e9
+        roof["spmv_residual"] = {"achieved": r_ach, "frac": r_ach / peak, "ms_per_launch": r_ms,
+                                 "bytes_per_launch": ab["resid_fine"]}
     # per-V-cycle aggregate fraction
     total_bytes_cycle = ab["resid_fine"] * 3 + ab.get("transfer", 0)
     if "lsolve_fine" in ab:
@@ -292,6 +300,22 @@ def main():
                               "rows_per_level_L": fs["rows_per_level_L"], "rows_per_level_U": fs["rows_per_level_U"],
                               "nnz_L": fs["nnz_L"], "nnz_U": fs["nnz_U"]}
     print(json.dumps(line), flush=True)
+
+
+NCU_KERNEL = {"lsolve_fine": "void unnamed>::k_chain<0>", "usolve_fine": "void unnamed>::k_chain<1>",
+              "gs_fine": "void unnamed>::k_chain<2>", "resid_fine": "void k_rowop<1, 1>"}
+
+
+def ncu_traffic(dom, args):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture
+    (profiles/round1/traffic.json, made by scripts/profile_round1.sh on the default workload)."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "round1", "traffic.json")
+    if args.config != 5 or args.smoother != "ilut" or not os.path.exists(path):
+        return None, None
+    rec = json.load(open(path)).get(NCU_KERNEL.get(dom, ""))
+    if not rec:
+        return None, None
+    return rec["dram_bytes_per_launch"], "profiles/round1/traffic.json (ncu --set full, config 5 ILUT)"
 
 
 def cpu_baseline(pb, H, args):
