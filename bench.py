@@ -39,6 +39,7 @@ def parse():
     ap.add_argument("--smoother", choices=["ilut", "gs"], default="ilut")
     ap.add_argument("--ordering", choices=["none", "rcm"], default="none")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-bicgstab", action="store_true", help="skip the BiCGSTAB sub-measurement")
     ap.add_argument("--cpu-sample-cycles", type=int, default=0, help="0: a full oracle solve")
     return ap.parse_args()
 
@@ -229,6 +230,24 @@ def main():
         e2e_c += r2.cycles
     e2e_val, _, T_e2e = job_throughput(float(n * e2e_c), sum(e2e_t), device="cuda")
 
+    # BiCGSTAB with the p-MG preconditioner, same system,
+    # device-resident vectors, device time of the Krylov loop (two V-cycles per iteration)
+    bicg = None
+    if not args.no_bicgstab:
+        bt, bit, brep = [], 0, None
+        for k in range(args.warmup + args.steps):
+            d_u.copy_(d_u0)
+            torch.cuda.synchronize()
+            brep = pmg.bicgstab_device(H, d_f.data_ptr(), d_u.data_ptr())
+            if k >= args.warmup:
+                bt.append(brep.solve_seconds)
+                bit += brep.iterations
+        bicg = {"ms_per_solve": 1e3 * sum(bt) / len(bt), "iterations": bit / len(bt),
+                "v_cycles_per_solve": 2 * bit / len(bt), "converged": bool(brep.converged),
+                "final_res": float(brep.residual_history[-1]),
+                "dof_it_per_s": float(n * bit / sum(bt)) if sum(bt) > 0 else None,
+                "note": "one iteration = two preconditioner V-cycles + two SpMVs + 4 dots"}
+
     if rank != 0:
         return
     # roofline of the dominant fine-level kernel class
@@ -293,6 +312,7 @@ def main():
         "kernel_ms": breakdown,
         "clocks": clk,
         "cpu_baseline": cpu,
+        "bicgstab": bicg,
     }
     if "factor_stats" in ab:
         fs = ab["factor_stats"]

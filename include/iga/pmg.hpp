@@ -105,6 +105,13 @@ struct SolveReport {
     double setup_seconds = 0, solve_seconds = 0;
 };
 
+struct KrylovReport {
+    int iterations = 0;
+    std::vector<double> residual_history;  // [0] = 1
+    bool converged = false, diverged = false, breakdown = false;
+    double solve_seconds = 0;
+};
+
 class PmgHierarchy {  // SPEC.md:313-316, immutable after construction
    public:
     pmg_hier handle() const { return h_.get(); }
@@ -119,6 +126,7 @@ class PmgHierarchy {  // SPEC.md:313-316, immutable after construction
     friend Vector restrict_(const PmgHierarchy&, int, const Vector&);
     friend void cycle(const PmgHierarchy&, int, Vector&, const Vector&);
     friend std::pair<Vector, SolveReport> solve(const PmgHierarchy&, const Vector&, double, int, const Vector*);
+    friend std::pair<Vector, KrylovReport> bicgstab(const PmgHierarchy&, const Vector&, double, int, const Vector*);
 };
 
 PmgHierarchy build_hierarchy(const HierarchyInputs& in, Smoother smoother = Smoother::ilut, int nu1 = 1, int nu2 = 1,
@@ -130,5 +138,9 @@ void cycle(const PmgHierarchy& H, int level, Vector& u, const Vector& f);       
 // SPEC.md:363-371; guess == nullptr -> zero initial guess
 std::pair<Vector, SolveReport> solve(const PmgHierarchy& H, const Vector& f, double tol = 1e-8, int max_cycles = 200,
                                      const Vector* guess = nullptr);
+// SPEC.md:269-277 with as_preconditioner(H): BiCGSTAB, one V-cycle from zero
+// per preconditioning phase; guess == nullptr -> zero initial guess
+std::pair<Vector, KrylovReport> bicgstab(const PmgHierarchy& H, const Vector& f, double tol = 1e-8, int max_iter = 200,
+                                         const Vector* guess = nullptr);
 
 }  // namespace iga

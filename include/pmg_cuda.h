@@ -39,7 +39,7 @@ enum {
 
 enum { PMG_SMOOTHER_ILUT = 0, PMG_SMOOTHER_GS = 1 };
 enum { PMG_ORDER_NONE = 0, PMG_ORDER_RCM = 1 };
-enum { PMG_FLAG_CONVERGED = 1, PMG_FLAG_DIVERGED = 2 };
+enum { PMG_FLAG_CONVERGED = 1, PMG_FLAG_DIVERGED = 2, PMG_FLAG_BREAKDOWN = 4 };
 
 /* read-only host CSR view (borrowed; copied at create) */
 typedef struct pmg_csr_view {
@@ -118,6 +118,16 @@ int pmg_solve(pmg_work W, const double* f, double* u_inout, double tol, int max_
 /* the same with device-resident f/u (pointers into device memory, e.g. torch tensors) */
 int pmg_solve_device(pmg_work W, const double* d_f, double* d_u, double tol, int max_cycles, double* rho_hist,
                      int* cycles, int* flags, double* solve_seconds);
+/* BiCGSTAB right-preconditioned by one
+ * V-cycle from zero guess per preconditioning phase (as_preconditioner).
+ * res_hist[0..*iters] receives ||r_i||/||f-Au_0|| of the recursively updated residual
+ * (res_hist[0] = 1; max_iter+1 entries); flags |= PMG_FLAG_CONVERGED / PMG_FLAG_DIVERGED /
+ * PMG_FLAG_BREAKDOWN (rho = 0, (rh,v) = 0 or omega = 0).  Replaces the
+ * reference's bicgstab(A, f, as_preconditioner(hier), tol, max_iter) -> (u, KrylovReport). */
+int pmg_bicgstab(pmg_work W, const double* f, double* u_inout, double tol, int max_iter, double* res_hist,
+                 int* iters, int* flags, double* solve_seconds);
+int pmg_bicgstab_device(pmg_work W, const double* d_f, double* d_u, double tol, int max_iter, double* res_hist,
+                        int* iters, int* flags, double* solve_seconds);
 /* one cycle at p-level `level` on host vectors (u updated in place) */
 int pmg_cycle(pmg_work W, int level, double* u, const double* f);
 /* prolongate: v_fine = ML_l^-1 P_l v_coarse; restrict */

@@ -59,6 +59,13 @@ static inline double row_dot(const int32_t* rp, const int32_t* ci, const double*
     return s;
 }
 
+// y = A x
+static void spmv_into(const Csr& A, const double* x, double* y) {
+    par_rows(A.n, [&](int32_t i0, int32_t i1) {
+        for (int32_t i = i0; i < i1; ++i) y[i] = row_dot(A.rp.data(), A.ci.data(), A.v.data(), i, x);
+    });
+}
+
 // r_i = f_i - (A x)_i
 static void residual(const Csr& A, const double* x, const double* f, double* r) {
     par_rows(A.n, [&](int32_t i0, int32_t i1) {
@@ -84,14 +91,15 @@ static double chunk_reduce(const double* v256) {
     }
     return c;
 }
-static double norm2(const double* r, int64_t n) {
+// (x, y) in the same canonical order, with products x_i * y_i in place of squares
+static double dot2(const double* x, const double* y, int64_t n) {
     int64_t nch = (n + 255) / 256;
     std::vector<double> part(nch);
     double buf[256];
     for (int64_t c = 0; c < nch; ++c) {
         for (int t = 0; t < 256; ++t) {
             int64_t i = c * 256 + t;
-            buf[t] = i < n ? r[i] * r[i] : 0.0;
+            buf[t] = i < n ? x[i] * y[i] : 0.0;
         }
         part[c] = chunk_reduce(buf);
     }
@@ -100,8 +108,9 @@ static double norm2(const double* r, int64_t n) {
         for (int64_t k = t; k < nch; k += 256) a = a + part[k];
         buf[t] = a;
     }
-    return std::sqrt(chunk_reduce(buf));
+    return chunk_reduce(buf);
 }
+static double norm2(const double* r, int64_t n) { return std::sqrt(dot2(r, r, n)); }
 
 // Forward lexicographic Gauss-Seidel, u_i <- ((f_i - S_L) - S_U) * (1/a_ii) with S_L over
 // j < i (new values) and S_U over j > i (old values), each ascending from +0
@@ -557,6 +566,82 @@ static int64_t vcycle(Hier& H, int l, double* u, const double* f, const double* 
     return -1;
 }
 
+// Right-preconditioned BiCGSTAB (one V-cycle per
+// preconditioning phase).  One iteration = one full step with two preconditioner applications;
+// the stop test uses the recursively updated residual, rho_i = ||r_i|| / ||f - A u0||.  Every
+// dot product and norm is canonical (dot2 / norm2) and every vector update has the fixed
+// operation order below, which the GPU path reproduces bit for bit:
+//   p = r (i = 1),  p = r + beta * (p - omega * v)      beta = (rho / rho_prev) * (alpha / omega)
+//   s = r - alpha * v;  u = (u + alpha * ph) + omega * sh;  r = s - omega * t
+// Breakdown (flag, stop): (rh, r) = 0, (rh, v) = 0, or omega = 0 after the update.
+template <class Prec>
+static int bicgstab(const Csr& A, const double* f, double* u, double tol, int max_iter, Prec&& prec, double* hist,
+                    int* iters, int* flags) {
+    const int32_t n = A.n;
+    std::vector<double> r(n), rh(n), p(n), v(n), s(n), t(n), ph(n), sh(n);
+    residual(A, u, f, r.data());
+    const double n0 = norm2(r.data(), n);
+    hist[0] = 1.0;
+    *iters = 0;
+    *flags = 0;
+    if (n0 == 0.0) {
+        *flags = PMG_FLAG_CONVERGED;
+        return PMG_OK;
+    }
+    rh = r;
+    double rho_prev = 1.0, alpha = 1.0, omega = 1.0;
+    for (int it = 1; it <= max_iter; ++it) {
+        const double rho = dot2(rh.data(), r.data(), n);
+        if (rho == 0.0 || !std::isfinite(rho)) {
+            *flags |= PMG_FLAG_BREAKDOWN;
+            break;
+        }
+        if (it == 1) {
+            p = r;
+        } else {
+            const double beta = (rho / rho_prev) * (alpha / omega);
+            for (int32_t i = 0; i < n; ++i) p[i] = r[i] + beta * (p[i] - omega * v[i]);
+        }
+        int rc = prec(p.data(), ph.data());
+        if (rc) return rc;
+        spmv_into(A, ph.data(), v.data());
+        const double rv = dot2(rh.data(), v.data(), n);
+        if (rv == 0.0 || !std::isfinite(rv)) {
+            *flags |= PMG_FLAG_BREAKDOWN;
+            break;
+        }
+        alpha = rho / rv;
+        for (int32_t i = 0; i < n; ++i) s[i] = r[i] - alpha * v[i];
+        rc = prec(s.data(), sh.data());
+        if (rc) return rc;
+        spmv_into(A, sh.data(), t.data());
+        const double tt = dot2(t.data(), t.data(), n);
+        const double ts = dot2(t.data(), s.data(), n);
+        omega = tt == 0.0 ? 0.0 : ts / tt;
+        for (int32_t i = 0; i < n; ++i) {
+            u[i] = (u[i] + alpha * ph[i]) + omega * sh[i];
+            r[i] = s[i] - omega * t[i];
+        }
+        const double res = norm2(r.data(), n) / n0;
+        hist[it] = res;
+        *iters = it;
+        if (res <= tol) {
+            *flags |= PMG_FLAG_CONVERGED;
+            break;
+        }
+        if (!(res <= 1e10)) {
+            *flags |= PMG_FLAG_DIVERGED;
+            break;
+        }
+        if (omega == 0.0) {
+            *flags |= PMG_FLAG_BREAKDOWN;
+            break;
+        }
+        rho_prev = rho;
+    }
+    return PMG_OK;
+}
+
 }  // namespace orc
 
 // =================================================================== C ABI
@@ -583,6 +668,7 @@ int orc_residual(const pmg_csr_view* A, const double* x, const double* f, double
     return PMG_OK;
 }
 double orc_norm2(const double* r, int64_t n) { return norm2(r, n); }
+double orc_dot(const double* x, const double* y, int64_t n) { return dot2(x, y, n); }
 int orc_gs_sweep(const pmg_csr_view* A, double* u, const double* f, int64_t* err_row) {
     if (A->nrows != A->ncols) return PMG_ERR_DIM;
     Csr c = Csr::from(*A);
@@ -776,6 +862,35 @@ int orc_solve(orc_hier h, const double* f, double* u, double tol, int max_cycles
     }
     if (solve_seconds) *solve_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     return rc;
+}
+
+// BiCGSTAB with one V-cycle from zero (right-hand side = the vector) as preconditioner
+int orc_bicgstab(orc_hier h, const double* f, double* u, double tol, int max_iter, double* hist, int* iters, int* flags,
+                 double* solve_seconds) {
+    Hier& H = h->H;
+    const int32_t n = H.pl[0].A.n;
+    auto t0 = std::chrono::steady_clock::now();
+    auto prec = [&](const double* x, double* z) {
+        std::fill(z, z + n, 0.0);
+        int64_t e = vcycle(H, 0, z, x, x, true);
+        return e >= 0 ? int(PMG_ZERO_DIAG) : int(PMG_OK);
+    };
+    int rc = bicgstab(H.pl[0].A, f, u, tol, max_iter, prec, hist, iters, flags);
+    if (solve_seconds) *solve_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return rc;
+}
+
+// BiCGSTAB without preconditioner (SPEC.md:277 example: SPD system vs a dense solve)
+int orc_bicgstab_plain(const pmg_csr_view* A, const double* f, double* u, double tol, int max_iter, double* hist,
+                       int* iters, int* flags) {
+    if (A->nrows != A->ncols) return PMG_ERR_DIM;
+    Csr c = Csr::from(*A);
+    const int32_t n = c.n;
+    auto prec = [&](const double* x, double* z) {
+        std::copy(x, x + n, z);
+        return int(PMG_OK);
+    };
+    return bicgstab(c, f, u, tol, max_iter, prec, hist, iters, flags);
 }
 
 int orc_cycle(orc_hier h, int level, double* u, const double* f) {

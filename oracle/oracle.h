@@ -9,6 +9,7 @@
  *   SPEC.md:242-250  rcm_ordering               SPEC.md:251-259  ilut_factorize (Saad ILUT, rules 1+2)
  *   SPEC.md:260-268  ilut_apply                 SPEC.md:336-353  prolongate / restrict (lumped L2)
  *   SPEC.md:354-371  cycle / solve (V(nu1,nu2), tol 1e-8, diverged > 1e10, max 200)
+ *   SPEC.md:269-277, :372-380  bicgstab with one V-cycle as preconditioner
  *   SPEC.md:317-320, :390-391  h-MG coarse correction (ILUT, knot-insertion P, P^T, dense LU at 2^-2)
  *   PAPER.md:196-226, :273-319  the algorithm
  * with the decisions SURVEY.md D1-D14 and the per-row operation orders of DESIGN.md §3.
@@ -63,6 +64,13 @@ orc_factor orc_hier_factor(orc_hier H, int which);
 int orc_solve(orc_hier H, const double* f, double* u, double tol, int max_cycles, double* rho_hist, int* cycles,
               int* flags, double* solve_seconds, double* setup_seconds);
 int orc_cycle(orc_hier H, int level, double* u, const double* f);
+/* right-preconditioned BiCGSTAB, one V-cycle from zero per preconditioning;
+ * hist needs max_iter+1 entries; flags: PMG_FLAG_CONVERGED / DIVERGED / BREAKDOWN */
+int orc_bicgstab(orc_hier H, const double* f, double* u, double tol, int max_iter, double* hist, int* iters, int* flags,
+                 double* solve_seconds);
+int orc_bicgstab_plain(const pmg_csr_view* A, const double* f, double* u, double tol, int max_iter, double* hist,
+                       int* iters, int* flags);
+double orc_dot(const double* x, const double* y, int64_t n); /* canonical order */
 
 #ifdef __cplusplus
 }

@@ -66,6 +66,10 @@ def lib():
         L.orc_hier_factor.restype = vp
         L.orc_solve.argtypes = [vp, vp, vp, dbl, ctypes.c_int, vp, vp, vp, vp, vp]
         L.orc_cycle.argtypes = [vp, ctypes.c_int, vp, vp]
+        L.orc_bicgstab.argtypes = [vp, vp, vp, dbl, ctypes.c_int, vp, vp, vp, vp]
+        L.orc_bicgstab_plain.argtypes = [vp, vp, vp, dbl, ctypes.c_int, vp, vp, vp]
+        L.orc_dot.restype = dbl
+        L.orc_dot.argtypes = [vp, vp, i64]
         _lib = L
     return _lib
 
@@ -107,6 +111,30 @@ def residual(A, x, f):
 def norm2(r):
     r = np.ascontiguousarray(r, float)
     return lib().orc_norm2(_p(r), r.size)
+
+
+def dot(x, y):
+    x, y = np.ascontiguousarray(x, float), np.ascontiguousarray(y, float)
+    return lib().orc_dot(_p(x), _p(y), x.size)
+
+
+def _krylov_report(iters, hist, flags, seconds=None):
+    it = iters.value
+    return dict(iterations=it, residual_history=hist[: it + 1].copy(), converged=bool(flags.value & 1),
+                diverged=bool(flags.value & 2), breakdown=bool(flags.value & 4), solve_seconds=seconds)
+
+
+def bicgstab_plain(A, f, u0=None, tol=1e-8, max_iter=200):
+    """Unpreconditioned BiCGSTAB, same arithmetic as the preconditioned one."""
+    f = np.ascontiguousarray(f, float)
+    u = np.zeros(f.size) if u0 is None else np.array(u0, dtype=float, copy=True)
+    hist = np.zeros(max_iter + 1)
+    it, flags = ctypes.c_int(), ctypes.c_int()
+    st = lib().orc_bicgstab_plain(ctypes.byref(view(A)), _p(f), _p(u), tol, max_iter, _p(hist), ctypes.byref(it),
+                                  ctypes.byref(flags))
+    if st != PMG_OK:
+        raise OracleError(st)
+    return u, _krylov_report(it, hist, flags)
 
 
 def gauss_seidel_sweep(A, u, f):
@@ -258,6 +286,17 @@ class Hierarchy:
         c = cyc.value
         return u, dict(cycles=c, residual_history=hist[: c + 1].copy(), converged=bool(flags.value & 1),
                        diverged=bool(flags.value & 2), solve_seconds=ts.value, setup_seconds=tsu.value)
+
+    def bicgstab(self, f, u0, tol=1e-8, max_iter=200):
+        """BiCGSTAB preconditioned by one V-cycle from zero."""
+        u = np.array(u0, dtype=float, copy=True)
+        hist = np.zeros(max_iter + 1)
+        it, flags, ts = ctypes.c_int(), ctypes.c_int(), ctypes.c_double()
+        st = lib().orc_bicgstab(self.h, _p(np.ascontiguousarray(f, float)), _p(u), tol, max_iter, _p(hist),
+                                ctypes.byref(it), ctypes.byref(flags), ctypes.byref(ts))
+        if st != PMG_OK:
+            raise OracleError(st)
+        return u, _krylov_report(it, hist, flags, ts.value)
 
     def cycle(self, u, f, level=0):
         u = np.array(u, dtype=float, copy=True)

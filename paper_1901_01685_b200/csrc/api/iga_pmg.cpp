@@ -230,4 +230,24 @@ std::pair<Vector, SolveReport> solve(const PmgHierarchy& H, const Vector& f, dou
     return {std::move(u), std::move(rep)};
 }
 
+std::pair<Vector, KrylovReport> bicgstab(const PmgHierarchy& H, const Vector& f, double tol, int max_iter,
+                                         const Vector* guess) {
+    need(f.size(), size_t(H.n_), "bicgstab");
+    Vector u = guess ? *guess : Vector(H.n_, 0.0);
+    need(u.size(), size_t(H.n_), "bicgstab");
+    auto w = make_work(H);
+    KrylovReport rep;
+    std::vector<double> hist(size_t(max_iter) + 1);
+    int iters = 0, flags = 0;
+    double secs = 0;
+    check(pmg_bicgstab(w.get(), f.data(), u.data(), tol, max_iter, hist.data(), &iters, &flags, &secs), "bicgstab");
+    rep.iterations = iters;
+    rep.residual_history.assign(hist.begin(), hist.begin() + iters + 1);
+    rep.converged = flags & PMG_FLAG_CONVERGED;
+    rep.diverged = flags & PMG_FLAG_DIVERGED;
+    rep.breakdown = flags & PMG_FLAG_BREAKDOWN;
+    rep.solve_seconds = secs;
+    return {std::move(u), std::move(rep)};
+}
+
 }  // namespace iga

@@ -3,6 +3,7 @@
 // solve runs in the kernels of sell.cu / trsv.cu / dense.cu; the host only sequences
 // launches on the work stream.
 #include <chrono>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -14,6 +15,7 @@
 #include "chain.cuh"
 #include "dense.cuh"
 #include "ilut.cuh"
+#include "krylov.cuh"
 #include "rcm.hpp"
 #include "skew.cuh"
 #include "sell.cuh"
@@ -408,6 +410,10 @@ struct pmg_work_s {
     double* dhist = nullptr;
     int hist_cap = 0;
     double* h_pinned = nullptr;
+    // BiCGSTAB vectors (allocated on first use): u, r, rh, p, v, s, t, ph, sh; dots
+    double* kv[9] = {};
+    double* kdot = nullptr;   // device: [rho, rv, tt, ts, ||r||]
+    double* kdot_h = nullptr; // pinned host copy
     // optional per-class event timing
     bool prof = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool;
@@ -439,6 +445,9 @@ struct pmg_work_s {
         cudaFree(norm0);
         cudaFree(dhist);
         cudaFreeHost(h_pinned);
+        for (double* v : kv) cudaFree(v);
+        cudaFree(kdot);
+        cudaFreeHost(kdot_h);
         for (auto& e : ev_pool) {
             cudaEventDestroy(e.first);
             cudaEventDestroy(e.second);
@@ -652,6 +661,139 @@ int solve_loop(pmg_work_s& W, const double* d_f, double tol, int max_cycles, dou
     W.collect();
     (void)n;
     return rc;
+}
+
+// Right-preconditioned BiCGSTAB, the preconditioner one
+// V-cycle from zero.  Same algorithm, breakdown rules and operation order as the oracle
+// (oracle/oracle.cpp bicgstab): canonical dots on the device, scalars formed on the host from
+// the (bit-identical) dot values, fused vector updates.  u = kv[0] on entry and exit.
+int bicgstab_loop(pmg_work_s& W, const double* d_f, double tol, int max_iter, double* hist, int* iters, int* flags,
+                  double* seconds) {
+    pmg_hier_s& H = *W.H;
+    pmg_csr_s* A = H.pl[0].A;
+    PWork& w0 = W.pw[0];
+    const int32_t n = A->A.n;
+    double *u = W.kv[0], *r = W.kv[1], *rh = W.kv[2], *p = W.kv[3], *v = W.kv[4], *s = W.kv[5], *t = W.kv[6],
+           *ph = W.kv[7], *sh = W.kv[8];
+    cudaEvent_t e0, e1;
+    PMG_CUDA(cudaEventCreate(&e0));
+    PMG_CUDA(cudaEventCreate(&e1));
+    PMG_CUDA(cudaEventRecord(e0, W.st));
+    auto fetch = [&](int k) {  // dot slots [0, k) to the host
+        PMG_CUDA(cudaMemcpyAsync(W.kdot_h, W.kdot, sizeof(double) * k, cudaMemcpyDeviceToHost, W.st));
+        PMG_CUDA(cudaStreamSynchronize(W.st));
+    };
+    auto dot = [&](const double* x, const double* y, int slot) {
+        NormCtx c = W.nc;
+        c.norm_out = W.kdot + slot;
+        c.n0 = nullptr;
+        c.hist_out = nullptr;
+        W.run(kClsMisc, 1, [&] { vec_dot(x, y, n, c, W.st); });
+    };
+    auto prec = [&](const double* x, double* z) {  // z = one V-cycle from zero with right-hand side x
+        w0.cur = 0;
+        W.run(kClsMisc, 0, [&] { PMG_CUDA(cudaMemsetAsync(w0.u[0], 0, sizeof(double) * n, W.st)); });
+        int rc = vcycle(W, 0, x, x, true);
+        W.run(kClsMisc, 0, [&] {
+            PMG_CUDA(cudaMemcpyAsync(z, w0.u[w0.cur], sizeof(double) * n, cudaMemcpyDeviceToDevice, W.st));
+        });
+        return rc;
+    };
+    auto spmv = [&](const double* x, double* y) {
+        W.run(kClsResid0, 1, [&] { sell_rowop(A->S, kOpSpmv, x, nullptr, nullptr, y, nullptr, W.st); });
+    };
+    NormCtx nc = W.nc;
+    nc.norm_out = W.kdot + 4;
+    nc.n0 = nullptr;
+    nc.hist_out = nullptr;
+    W.run(kClsResid0, 1, [&] { sell_rowop(A->S, kOpResidual, u, d_f, nullptr, r, &nc, W.st); });
+    PMG_CUDA(cudaMemcpyAsync(W.kdot_h + 4, W.kdot + 4, sizeof(double), cudaMemcpyDeviceToHost, W.st));
+    PMG_CUDA(cudaStreamSynchronize(W.st));
+    const double n0 = W.kdot_h[4];
+    hist[0] = 1.0;
+    *iters = 0;
+    *flags = 0;
+    int rc = PMG_OK;
+    if (n0 == 0.0) {
+        *flags = PMG_FLAG_CONVERGED;
+    } else {
+        PMG_CUDA(cudaMemcpyAsync(rh, r, sizeof(double) * n, cudaMemcpyDeviceToDevice, W.st));
+        double rho_prev = 1.0, alpha = 1.0, omega = 1.0;
+        for (int it = 1; it <= max_iter; ++it) {
+            dot(rh, r, 0);
+            fetch(1);
+            const double rho = W.kdot_h[0];
+            if (rho == 0.0 || !std::isfinite(rho)) {
+                *flags |= PMG_FLAG_BREAKDOWN;
+                break;
+            }
+            if (it == 1) {
+                PMG_CUDA(cudaMemcpyAsync(p, r, sizeof(double) * n, cudaMemcpyDeviceToDevice, W.st));
+            } else {
+                const double beta = (rho / rho_prev) * (alpha / omega);
+                W.run(kClsMisc, 1, [&] { bicg_update_p(p, r, v, beta, omega, n, W.st); });
+            }
+            if ((rc = prec(p, ph))) break;
+            spmv(ph, v);
+            dot(rh, v, 1);
+            fetch(2);
+            const double rv = W.kdot_h[1];
+            if (rv == 0.0 || !std::isfinite(rv)) {
+                *flags |= PMG_FLAG_BREAKDOWN;
+                break;
+            }
+            alpha = rho / rv;
+            W.run(kClsMisc, 1, [&] { bicg_update_s(s, r, v, alpha, n, W.st); });
+            if ((rc = prec(s, sh))) break;
+            spmv(sh, t);
+            dot(t, t, 2);
+            dot(t, s, 3);
+            fetch(4);
+            const double tt = W.kdot_h[2], ts = W.kdot_h[3];
+            omega = tt == 0.0 ? 0.0 : ts / tt;
+            W.run(kClsMisc, 1, [&] { bicg_update_ur(u, r, s, t, ph, sh, alpha, omega, n, W.st); });
+            NormCtx nr = W.nc;
+            nr.norm_out = W.kdot + 4;
+            nr.n0 = nullptr;
+            nr.hist_out = nullptr;
+            W.run(kClsMisc, 1, [&] { vec_norm(r, n, nr, W.st); });
+            PMG_CUDA(cudaMemcpyAsync(W.kdot_h + 4, W.kdot + 4, sizeof(double), cudaMemcpyDeviceToHost, W.st));
+            PMG_CUDA(cudaStreamSynchronize(W.st));
+            const double res = W.kdot_h[4] / n0;
+            hist[it] = res;
+            *iters = it;
+            if (res <= tol) {
+                *flags |= PMG_FLAG_CONVERGED;
+                break;
+            }
+            if (!(res <= 1e10)) {
+                *flags |= PMG_FLAG_DIVERGED;
+                break;
+            }
+            if (omega == 0.0) {
+                *flags |= PMG_FLAG_BREAKDOWN;
+                break;
+            }
+            rho_prev = rho;
+        }
+    }
+    PMG_CUDA(cudaEventRecord(e1, W.st));
+    PMG_CUDA(cudaEventSynchronize(e1));
+    float ms = 0;
+    PMG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    if (seconds) *seconds = ms * 1e-3;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    W.collect();
+    return rc;
+}
+
+void ensure_krylov(pmg_work_s& W) {
+    if (W.kdot) return;
+    const int32_t n = W.H->pl[0].A->A.n;
+    for (double*& v : W.kv) v = dalloc<double>(n);
+    W.kdot = dalloc<double>(8);
+    PMG_CUDA(cudaMallocHost(&W.kdot_h, sizeof(double) * 8));
 }
 
 }  // namespace
@@ -1029,6 +1171,36 @@ int pmg_solve(pmg_work W, const double* f, double* u_inout, double tol, int max_
         PMG_CUDA(cudaMemcpyAsync(w0.u[0], u_inout, sizeof(double) * n, cudaMemcpyHostToDevice, W->st));
         int rc = solve_loop(*W, w0.f, tol, max_cycles, rho_hist, cycles, flags, solve_seconds);
         PMG_CUDA(cudaMemcpyAsync(u_inout, w0.u[w0.cur], sizeof(double) * n, cudaMemcpyDeviceToHost, W->st));
+        PMG_CUDA(cudaStreamSynchronize(W->st));
+        return rc;
+    });
+}
+
+int pmg_bicgstab_device(pmg_work W, const double* d_f, double* d_u, double tol, int max_iter, double* res_hist,
+                        int* iters, int* flags, double* solve_seconds) {
+    return guarded([&] {
+        if (max_iter < 0) throw ArgError("max_iter < 0", PMG_ERR_ARG);
+        ensure_krylov(*W);
+        const int32_t n = W->H->pl[0].A->A.n;
+        PMG_CUDA(cudaMemcpyAsync(W->kv[0], d_u, sizeof(double) * n, cudaMemcpyDeviceToDevice, W->st));
+        int rc = bicgstab_loop(*W, d_f, tol, max_iter, res_hist, iters, flags, solve_seconds);
+        PMG_CUDA(cudaMemcpyAsync(d_u, W->kv[0], sizeof(double) * n, cudaMemcpyDeviceToDevice, W->st));
+        PMG_CUDA(cudaStreamSynchronize(W->st));
+        return rc;
+    });
+}
+
+int pmg_bicgstab(pmg_work W, const double* f, double* u_inout, double tol, int max_iter, double* res_hist, int* iters,
+                 int* flags, double* solve_seconds) {
+    return guarded([&] {
+        if (max_iter < 0) throw ArgError("max_iter < 0", PMG_ERR_ARG);
+        ensure_krylov(*W);
+        const int32_t n = W->H->pl[0].A->A.n;
+        PWork& w0 = W->pw[0];
+        PMG_CUDA(cudaMemcpyAsync(w0.f, f, sizeof(double) * n, cudaMemcpyHostToDevice, W->st));
+        PMG_CUDA(cudaMemcpyAsync(W->kv[0], u_inout, sizeof(double) * n, cudaMemcpyHostToDevice, W->st));
+        int rc = bicgstab_loop(*W, w0.f, tol, max_iter, res_hist, iters, flags, solve_seconds);
+        PMG_CUDA(cudaMemcpyAsync(u_inout, W->kv[0], sizeof(double) * n, cudaMemcpyDeviceToHost, W->st));
         PMG_CUDA(cudaStreamSynchronize(W->st));
         return rc;
     });

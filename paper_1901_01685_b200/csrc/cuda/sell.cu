@@ -132,17 +132,17 @@ __device__ void norm_finalize(const NormCtx& c, int nblocks) {
     if (threadIdx.x == 0) {
         double t = wsum[0];
         for (int w = 1; w < 8; ++w) t = t + wsum[w];
-        double nrm = sqrt(t);
+        double nrm = c.raw ? t : sqrt(t);
         if (c.norm_out) c.norm_out[0] = nrm;
         if (c.hist_out) c.hist_out[0] = nrm / c.n0[0];
         *c.counter = 0u;
     }
 }
 
-// sum of squares of the block's 256 values in the canonical chunk order
-__device__ __forceinline__ void block_sq_partial(double v, const NormCtx& c) {
+// sum of the block's 256 terms (squares, or products for a dot) in the canonical chunk order
+__device__ __forceinline__ void block_partial(double v, const NormCtx& c) {
     __shared__ double ws[8];
-    v = warp_butterfly(v * v);
+    v = warp_butterfly(v);
     if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = v;
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -152,6 +152,7 @@ __device__ __forceinline__ void block_sq_partial(double v, const NormCtx& c) {
     }
     norm_finalize(c, gridDim.x);
 }
+__device__ __forceinline__ void block_sq_partial(double v, const NormCtx& c) { block_partial(v * v, c); }
 
 template <int OP, bool NORM>
 __global__ void __launch_bounds__(256) k_rowop(Sell S, const double* __restrict__ x, const double* __restrict__ f,
@@ -211,6 +212,18 @@ __global__ void __launch_bounds__(256) k_vec_norm(const double* __restrict__ v, 
 
 void vec_norm(const double* v, int32_t n, const NormCtx& ctx, cudaStream_t st) {
     k_vec_norm<<<ceil_div(n, 256), 256, 0, st>>>(v, n, ctx);
+    PMG_LAUNCH_CHECK();
+}
+
+__global__ void __launch_bounds__(256) k_vec_dot(const double* __restrict__ x, const double* __restrict__ y, int32_t n,
+                                                 NormCtx nc) {
+    int32_t i = blockIdx.x * 256 + threadIdx.x;
+    block_partial(i < n ? x[i] * y[i] : 0.0, nc);
+}
+
+void vec_dot(const double* x, const double* y, int32_t n, NormCtx ctx, cudaStream_t st) {
+    ctx.raw = true;
+    k_vec_dot<<<ceil_div(n, 256), 256, 0, st>>>(x, y, n, ctx);
     PMG_LAUNCH_CHECK();
 }
 

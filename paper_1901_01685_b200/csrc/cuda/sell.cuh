@@ -55,6 +55,7 @@ struct NormCtx {
     double* norm_out = nullptr;   // ||y||_2
     const double* n0 = nullptr;   // if set: hist_out = norm / *n0
     double* hist_out = nullptr;
+    bool raw = false;             // write the canonical sum itself (a dot product), no sqrt
 };
 
 void sell_rowop(const Sell& S, RowOp op, const double* x, const double* f, const double* ml, double* y,
@@ -62,6 +63,8 @@ void sell_rowop(const Sell& S, RowOp op, const double* x, const double* f, const
 
 // canonical norm of a plain vector (same reduction tree as the fused residual norm)
 void vec_norm(const double* v, int32_t n, const NormCtx& ctx, cudaStream_t st);
+// canonical dot product (x, y): the same tree over the products x_i * y_i (ctx.raw forced)
+void vec_dot(const double* x, const double* y, int32_t n, NormCtx ctx, cudaStream_t st);
 
 void fill_value(double* v, int64_t n, double value_bits_as_double, cudaStream_t st);
 void fill_sentinel(double* v, int64_t n, cudaStream_t st);

@@ -109,6 +109,8 @@ def lib():
         L.pmg_solve.argtypes = [vp, vp, vp, dbl, ci, vp, vp, vp, vp]
         L.pmg_solve_device.argtypes = [vp, vp, vp, dbl, ci, vp, vp, vp, vp]
         L.pmg_cycle.argtypes = [vp, ci, vp, vp]
+        L.pmg_bicgstab.argtypes = [vp, vp, vp, dbl, ci, vp, vp, vp, vp]
+        L.pmg_bicgstab_device.argtypes = [vp, vp, vp, dbl, ci, vp, vp, vp, vp]
         L.pmg_prolongate.argtypes = [vp, ci, vp, vp]
         L.pmg_restrict.argtypes = [vp, ci, vp, vp]
         L.pmg_work_kernel_times.argtypes = [vp, vp, ci]
@@ -284,6 +286,18 @@ class SolveReport:
     extra: dict = field(default_factory=dict)
 
 
+@dataclass
+class KrylovReport:
+    """SPEC.md:218-221: iterations, residual_history ([0] = 1), converged, breakdown."""
+
+    iterations: int
+    residual_history: np.ndarray
+    converged: bool
+    diverged: bool
+    breakdown: bool
+    solve_seconds: float
+
+
 class PmgHierarchy:
     """Immutable device hierarchy: p-levels with smoother state and lumped
     L2 transfers, and the p=1 h-multigrid chain with a dense coarsest solve."""
@@ -397,6 +411,33 @@ def solve(hier: PmgHierarchy, f, tol=1e-8, max_cycles=200, guess=None):
     c = cyc.value
     return u, SolveReport(c, hist[: c + 1].copy(), bool(flags.value & 1), bool(flags.value & 2), hier.setup_seconds,
                           secs.value)
+
+
+def bicgstab(hier: PmgHierarchy, f, tol=1e-8, max_iter=200, guess=None):
+    """BiCGSTAB preconditioned by one V-cycle of `hier` (SPEC.md:269-277 with
+    as_preconditioner, SPEC.md:372-380). Returns (u, KrylovReport)."""
+    f = _f64(f, hier.n)
+    u = np.zeros(hier.n) if guess is None else np.array(_f64(guess, hier.n), copy=True)
+    hist = np.zeros(max_iter + 1)
+    it, flags, secs = ctypes.c_int(), ctypes.c_int(), ctypes.c_double()
+    st = lib().pmg_bicgstab(hier.w, ptr(f), ptr(u), tol, max_iter, ptr(hist), ctypes.byref(it), ctypes.byref(flags),
+                            ctypes.byref(secs))
+    _raise(st, what="bicgstab")
+    k = it.value
+    return u, KrylovReport(k, hist[: k + 1].copy(), bool(flags.value & 1), bool(flags.value & 2),
+                           bool(flags.value & 4), secs.value)
+
+
+def bicgstab_device(hier: PmgHierarchy, d_f: int, d_u: int, tol=1e-8, max_iter=200):
+    """BiCGSTAB on device-resident vectors (raw device pointers)."""
+    hist = np.zeros(max_iter + 1)
+    it, flags, secs = ctypes.c_int(), ctypes.c_int(), ctypes.c_double()
+    st = lib().pmg_bicgstab_device(hier.w, ctypes.c_void_p(d_f), ctypes.c_void_p(d_u), tol, max_iter, ptr(hist),
+                                   ctypes.byref(it), ctypes.byref(flags), ctypes.byref(secs))
+    _raise(st, what="bicgstab_device")
+    k = it.value
+    return KrylovReport(k, hist[: k + 1].copy(), bool(flags.value & 1), bool(flags.value & 2), bool(flags.value & 4),
+                        secs.value)
 
 
 def solve_device(hier: PmgHierarchy, d_f: int, d_u: int, tol=1e-8, max_cycles=200):
