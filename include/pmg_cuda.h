@@ -72,6 +72,10 @@ int pmg_ilut_apply(pmg_factor F, const double* r, double* e);                   
 /* factor introspection: nnz, level counts (north star: level count + rows/level) */
 int pmg_factor_stats(pmg_factor F, int64_t* nnz_L, int64_t* nnz_U, int32_t* levels_L, int32_t* levels_U,
                      int32_t* max_row_L, int32_t* max_row_U);
+/* which sweep kernels apply_factor uses for F (no reference counterpart; reporting):
+ * level-scheduled, chained segments (seg = grid-row length) or skewed warps (lane skew D) */
+enum { PMG_SWEEP_LEVELS = 0, PMG_SWEEP_CHAIN = 1, PMG_SWEEP_SKEW = 2 };
+int pmg_factor_sweep_info(pmg_factor F, int32_t* kind, int32_t* seg, int32_t* skew_D_L, int32_t* skew_D_U);
 /* copy factors to host CSR arrays (L strictly lower, unit diagonal implicit; U with
  * diagonal); pass NULL arrays to query sizes only.  perm may be NULL. */
 int pmg_factor_export(pmg_factor F, int32_t* L_rowptr, int32_t* L_col, double* L_val, int32_t* U_rowptr,
@@ -143,6 +147,8 @@ int pmg_work_kernel_times(pmg_work W, double* ms_by_class, int n_classes);
  * finisher start, finisher end, helper value spins, finisher batch waits) and returns the
  * number of segments */
 int pmg_debug_chain_trace(int mode, unsigned long long* out, int cap);
+/* the same for the skewed-warp sweeps: 4 u64 per 32-segment warp block */
+int pmg_debug_skew_trace(int mode, unsigned long long* out, int cap);
 
 #ifdef __cplusplus
 }

@@ -162,6 +162,8 @@ struct pmg_factor_s {
         cudaFree(rev);
         cudaFree(splitL);
         cudaFree(splitU);
+        skew_plan_free(planL);
+        skew_plan_free(planU);
     }
 };
 
@@ -170,9 +172,9 @@ namespace {
 // e = U^{-1} L^{-1} r[perm] added into u[perm]  (y, x: scratch)
 void apply_factor(pmg_factor_s* F, const double* r, double* y, double* x, double* u, int* ticket, cudaStream_t st) {
     if (F->skew) {
-        SkewOp l{kSkewL, &F->Ls, nullptr, F->perm, r, y, nullptr, F->seg, F->planL.D};
+        SkewOp l{kSkewL, &F->planL, r, y, nullptr};
         skew_sweep(l, ticket, st);
-        SkewOp up{kSkewU, &F->Us, F->Udiag, F->perm, y, x, u, F->seg, F->planU.D};
+        SkewOp up{kSkewU, &F->planU, y, x, u};
         skew_sweep(up, ticket, st);
     } else if (F->seg > 0) {
         ChainOp l{kChainL, &F->Ls, nullptr, nullptr, F->splitL, F->perm, r, nullptr, y, nullptr, F->seg, F->bs, F->gapL};
@@ -327,10 +329,20 @@ int make_factor(pmg_csr_s* A, double tau, double fillfactor, int ordering, pmg_f
     // short rows (p=1 factors): the per-segment lag is dominated by the finisher batch
     F->bs = std::max(F->max_row_L, F->max_row_U) <= 16 ? 8 : 32;
     if (const char* e = getenv("PMG_CHAIN_BS")) F->bs = atoi(e);
-    if (F->seg > 0 && env_flag("PMG_SKEW")) {  // experimental, off by default
-        const bool okL = skew_plan(F->Ls, F->seg, kSkewL, F->max_row_L, F->planL, st);
-        const bool okU = skew_plan(F->Us, F->seg, kSkewU, F->max_row_U - 1, F->planU, st);
+    // short rows and reach (the p=1 h-levels): skewed-warp sweeps (skew.cu); PMG_SKEW=0 keeps
+    // the chained-segment kernel for every factor
+    const char* sk = getenv("PMG_SKEW");
+    if (F->seg > 0 && !F->perm && !(sk && sk[0] == '0') && F->max_row_L <= kSkewSlots &&
+        F->max_row_U - 1 <= kSkewSlots) {
+        const bool okL = skew_plan(F->Ls, nullptr, F->seg, kSkewL, F->planL, st);
+        const bool okU = okL && skew_plan(F->Us, F->Udiag, F->seg, kSkewU, F->planU, st);
         F->skew = okL && okU;
+        if (!F->skew) {
+            skew_plan_free(F->planL);
+            skew_plan_free(F->planU);
+        }
+        if (getenv("PMG_VERBOSE"))
+            fprintf(stderr, "[pmg] factor n=%d skew %d D %d/%d\n", F->n, int(F->skew), F->planL.D, F->planU.D);
     }
     *out = F.release();
     return PMG_OK;
@@ -500,11 +512,11 @@ void smooth_ilut(pmg_work_s& W, pmg_csr_s* A, pmg_factor_s* F, double* u, const 
     }
     if (F->skew) {
         W.run(fine ? kClsL0 : kClsCoarse, 4, [&] {
-            SkewOp l{kSkewL, &F->Ls, nullptr, F->perm, rr, y, nullptr, F->seg, F->planL.D};
+            SkewOp l{kSkewL, &F->planL, rr, y, nullptr};
             skew_sweep(l, W.ticket, W.st);
         });
         W.run(fine ? kClsU0 : kClsCoarse, 4, [&] {
-            SkewOp up{kSkewU, &F->Us, F->Udiag, F->perm, y, x, u, F->seg, F->planU.D};
+            SkewOp up{kSkewU, &F->planU, y, x, u};
             skew_sweep(up, W.ticket, W.st);
         });
     } else if (F->seg > 0) {
@@ -968,6 +980,14 @@ int pmg_factor_stats(pmg_factor F, int64_t* nnz_L, int64_t* nnz_U, int32_t* leve
     return PMG_OK;
 }
 
+int pmg_factor_sweep_info(pmg_factor F, int32_t* kind, int32_t* seg, int32_t* skew_D_L, int32_t* skew_D_U) {
+    if (kind) *kind = F->skew ? PMG_SWEEP_SKEW : F->seg > 0 ? PMG_SWEEP_CHAIN : PMG_SWEEP_LEVELS;
+    if (seg) *seg = F->seg;
+    if (skew_D_L) *skew_D_L = F->skew ? F->planL.D : 0;
+    if (skew_D_U) *skew_D_U = F->skew ? F->planU.D : 0;
+    return PMG_OK;
+}
+
 int pmg_factor_export(pmg_factor F, int32_t* Lrp, int32_t* Lc, double* Lv, int32_t* Urp, int32_t* Uc, double* Uv,
                       int32_t* perm) {
     return guarded([&] {
@@ -1272,6 +1292,19 @@ int pmg_debug_chain_trace(int mode, unsigned long long* out, int cap) {
     if (cudaDeviceSynchronize() != cudaSuccess) return -1;
     if (cudaMemcpy(out, g_chain_trace, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
     return g_chain_trace_n;
+}
+
+// diagnostics: the same for the skewed-warp sweeps (4 u64 per warp block); returns #blocks
+int pmg_debug_skew_trace(int mode, unsigned long long* out, int cap) {
+    if (mode == 1 || mode == 0) {
+        g_skew_trace_on = mode == 1;
+        return 0;
+    }
+    if (!g_skew_trace || !out) return 0;
+    const int n = std::min(g_skew_trace_n * 4, cap);
+    if (cudaDeviceSynchronize() != cudaSuccess) return -1;
+    if (cudaMemcpy(out, g_skew_trace, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+    return g_skew_trace_n;
 }
 
 // ms_by_class[0..6]: resid(A_p), L-solve(p), U-solve(p), GS(p), p-transfers, coarse (p<finest and

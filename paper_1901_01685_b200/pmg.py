@@ -99,6 +99,7 @@ def lib():
         L.pmg_factor_destroy.argtypes = [vp]
         L.pmg_ilut_apply.argtypes = [vp, vp, vp]
         L.pmg_factor_stats.argtypes = [vp, vp, vp, vp, vp, vp, vp]
+        L.pmg_factor_sweep_info.argtypes = [vp, vp, vp, vp, vp]
         L.pmg_factor_export.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp]
         L.pmg_hier_create.argtypes = [vp, P(vp), vp, vp]
         L.pmg_hier_destroy.argtypes = [vp]
@@ -228,9 +229,12 @@ class IlutFactorization:
         lib().pmg_factor_stats(self.h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c), ctypes.byref(d),
                                ctypes.byref(e), ctypes.byref(f))
         n = self.n
+        k, sg, dl, du = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        lib().pmg_factor_sweep_info(self.h, ctypes.byref(k), ctypes.byref(sg), ctypes.byref(dl), ctypes.byref(du))
         return dict(nnz_L=a.value, nnz_U=b.value, levels_L=c.value, levels_U=d.value,
                     rows_per_level_L=n / max(c.value, 1), rows_per_level_U=n / max(d.value, 1),
-                    max_row_L=e.value, max_row_U=f.value)
+                    max_row_L=e.value, max_row_U=f.value,
+                    sweep=("levels", "chain", "skew")[k.value], segment=sg.value, skew_D=(dl.value, du.value))
 
     def export(self):
         s = self.stats()

@@ -17,15 +17,15 @@ pytestmark = pytest.mark.gpu
 
 @pytest.fixture(params=["chain", "skew+chain", "levelsched"])
 def sweep_path(request, monkeypatch):
-    """Every sweep implementation must match the oracle: the chained-segment wavefront
-    (default for tensor-grid orderings), the experimental skewed-warp kernel for short-row
-    factors (PMG_SKEW=1) and the level-scheduled fallback."""
+    """Every sweep implementation must match the oracle: the default (skewed-warp kernel for
+    the short-row p=1 factors, chained-segment wavefront for the rest), the chained-segment
+    kernel for every factor (PMG_SKEW=0) and the level-scheduled fallback."""
     monkeypatch.delenv("PMG_FORCE_LEVELSCHED", raising=False)
     monkeypatch.delenv("PMG_SKEW", raising=False)
     if request.param == "levelsched":
         monkeypatch.setenv("PMG_FORCE_LEVELSCHED", "1")
-    elif request.param == "skew+chain":
-        monkeypatch.setenv("PMG_SKEW", "1")
+    elif request.param == "chain":
+        monkeypatch.setenv("PMG_SKEW", "0")
     return request.param
 
 RTOL_RHO = 1e-10
@@ -133,3 +133,22 @@ def test_solve_config2(degree, smoother, sweep_path):
 def test_solve_config3(sweep_path):
     rep, _ = _solve_parity(problem(3), "ilut")
     assert rep.converged
+
+
+@pytest.mark.parametrize("h_exp", [5, 6, 8])
+@pytest.mark.parametrize("geometry", ["square", "annulus"])
+def test_skew_sweeps_p1(h_exp, geometry, monkeypatch):
+    """The skewed-warp sweeps (skew.cu) on p=1 factors: one warp block (h=2^-5: 33 segments
+    -> 2 blocks), several blocks with halo hand-offs (2^-6, 2^-8), bitwise against the oracle."""
+    monkeypatch.delenv("PMG_SKEW", raising=False)
+    monkeypatch.delenv("PMG_FORCE_LEVELSCHED", raising=False)
+    spec = P.make_spec(geometry=geometry, rhs="one", degrees=(2, 1), h_exp=h_exp)
+    A = P.build(spec).hlevels[0].A
+    Fg = pmg.ilut_factorize(A, 1e-12, 1.0, "none")
+    st = Fg.stats()
+    assert st["sweep"] == "skew", st
+    Fo = O.ilut_factorize(A, 1e-12, 1.0, O.ORDER_NONE)
+    rng = np.random.default_rng(h_exp)
+    for _ in range(3):
+        r = rng.uniform(-1, 1, A.nrows)
+        assert_bitwise(pmg.ilut_apply(Fg, r), Fo.apply(r), "skew ilut_apply")
