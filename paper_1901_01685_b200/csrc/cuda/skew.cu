@@ -59,7 +59,9 @@ struct SkewSmem {
     uint4 item[PF][ICH][32];  // [step slot][16-B chunk][lane]: conflict-free 128-bit reads
     double rhs[PF][32];
     double Y[SPW + 1][RYS];   // row 0: halo (previous block's last segment); row k+1: segment k
-    unsigned long long bar[NG];
+    unsigned long long bar[NG];     // items of a group have landed (bulk copy)
+    unsigned long long rfull[NG];   // right-hand sides of a group are in (stager warp)
+    unsigned long long rempty[NG];  // a group's slots were consumed (sweep warp)
     int halo_ready;           // halo values [0, halo_ready) are in
     int cons_ix;              // segment 0's current row (halo ring reuse)
     int blk;
@@ -107,6 +109,9 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned b
                  "l"(src), "r"(bytes), "r"(smem_u32(b))
                  : "memory");
 }
+__device__ __forceinline__ void bar_arrive(unsigned long long* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
 __device__ __forceinline__ void bar_wait(unsigned long long* b, unsigned parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n"
@@ -124,17 +129,13 @@ __device__ __forceinline__ void st_rel_cta(int* p, int v) {
 }
 __device__ __forceinline__ int ld_vol_s(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
 
-template <int K>
-__global__ void __launch_bounds__(64) k_skew(SkewArgs a) {
+template <int K, bool TR>
+__global__ void __launch_bounds__(96) k_skew(SkewArgs a) {
     extern __shared__ __align__(128) unsigned char skew_smem[];
     SkewSmem& sm = *reinterpret_cast<SkewSmem*>(skew_smem);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n = a.n, S = a.seg, D = a.D;
-    if (threadIdx.x == 0) {
-        for (int q = 0; q < NG; ++q) bar_init(&sm.bar[q]);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    unsigned gbase = 0;  // bulk-copy groups issued by earlier blocks (mbarrier phases)
+    constexpr unsigned gbase = 0;  // barriers are re-initialised per block: group q <-> slot q % NG
 
     for (;;) {
         __syncthreads();
@@ -142,20 +143,46 @@ __global__ void __launch_bounds__(64) k_skew(SkewArgs a) {
             sm.blk = atomicAdd(a.ticket, 1);
             sm.halo_ready = 0;
             sm.cons_ix = -P;
+            // every copy / arrival of the previous block has been waited for or has completed
+            for (int q = 0; q < NG; ++q) {
+                bar_init(&sm.bar[q]);
+                bar_init(&sm.rfull[q]);
+                bar_init(&sm.rempty[q]);
+            }
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
-        for (int q = threadIdx.x; q < (SPW + 1) * RYS; q += 64) (&sm.Y[0][0])[q] = 0.0;
+        for (int q = threadIdx.x; q < (SPW + 1) * RYS; q += 96) (&sm.Y[0][0])[q] = 0.0;
         __syncthreads();
         const int blk = sm.blk;
         const int g0 = blk * SPW;
         if (g0 >= a.nseg) break;
-        if (a.trace && threadIdx.x == 0) a.trace[blk * 4 + 0] = gtimer();
+        if (TR && a.trace && threadIdx.x == 0) a.trace[blk * 8 + 0] = gtimer();
         const int kmax = min(SPW - 1, a.nseg - 1 - g0);
         const int T = S + kmax * D;
         const int NS = T + P;                       // steps of this block (t = tau + P)
         const unsigned nq = (NS + G - 1) / G;       // bulk-copy groups of this block
 
+        if (warp == 2) {
+            // ---------------------------------------------------------------- stager
+            // right-hand sides of the stage-0 rows, group by group, into the rhs ring
+            for (unsigned q = 0; q < nq; ++q) {
+                const unsigned Q = gbase + q, slot = Q % NG, use = Q / NG;
+                if (use > 0) bar_wait(&sm.rempty[slot], (use - 1) & 1);
+#pragma unroll
+                for (int e0 = 0; e0 < G * SPW; e0 += 32) {
+                    const int e = e0 + lane, st = int(q) * G + e / SPW, kk = e % SPW;
+                    const int gg = g0 + kk, ix = st - P - D * kk;
+                    const int64_t lo2 = int64_t(gg) * S;
+                    const bool in = gg < a.nseg && ix >= 0 && ix < S && lo2 + ix < n;
+                    const int64_t v = lo2 + ix;
+                    sm.rhs[slot * G + e / SPW][kk * NR] = in ? a.rhs[K == kSkewL ? v : int64_t(n) - 1 - v] : 0.0;
+                }
+                __syncwarp();
+                if (lane == 0) bar_arrive(&sm.rfull[slot]);
+            }
+            continue;
+        }
         if (warp == 1) {
-            gbase += nq;
             // ---------------------------------------------------------------- bridge
             // previous block's last segment -> halo ring, in order, as its values appear
             if (g0 > 0) {
@@ -170,6 +197,7 @@ __global__ void __launch_bounds__(64) k_skew(SkewArgs a) {
                     const unsigned ok = __ballot_sync(FULL, !is_sentinel(v));
                     const int cnt = ok == FULL ? 32 : __ffs(~ok) - 1;
                     if (lane < cnt) sm.Y[0][j & (RY - 1)] = v;
+                    if (TR && a.trace && lane < cnt && j == 200) a.trace[(blk - 1) * 8 + 5] = gtimer();
                     __syncwarp();
                     if (cnt > 0) {
                         if (lane == 0) st_rel_cta(&sm.halo_ready, j0 + cnt);
@@ -179,7 +207,7 @@ __global__ void __launch_bounds__(64) k_skew(SkewArgs a) {
                         __nanosleep(ns);
                         ns = min(ns * 2, 256u);
                     }
-                    if (a.trace && lane == 0) a.trace[blk * 4 + 3]++;
+                    if (TR && a.trace && lane == 0) a.trace[blk * 8 + 3]++;
                 }
             }
             continue;
@@ -198,22 +226,7 @@ __global__ void __launch_bounds__(64) k_skew(SkewArgs a) {
                 bulk_load(&sm.item[slot * G][0][0], bsrc + int64_t(q) * G * STEP_BYTES, bytes, &sm.bar[slot]);
             }
         };
-        auto rhs_issue = [&](int t) {  // right-hand side of step t's row (stage-0 lanes)
-            const int ix = t - P - D * k;
-            const bool in = role == 0 && ix >= 0 && ix < rows;
-            const int64_t v = lo + ix;
-            const double* rs = in ? a.rhs + (K == kSkewL ? v : int64_t(n) - 1 - v) : a.rhs;
-            cp_async8_z(&sm.rhs[t & (PF - 1)][lane], rs, in ? 8 : 0);
-            cp_commit();
-        };
-        auto group_wait = [&](int t) {  // items of step t have landed
-            if (t % G == 0 && t < NS) {
-                const unsigned q = unsigned(t) / G;
-                bar_wait(&sm.bar[(gbase + q) % NG], ((gbase + q) / NG) & 1);
-            }
-        };
         for (unsigned q = 0; q < NG; ++q) refill(q);
-        for (int t = 0; t < PF - 1; ++t) rhs_issue(t);
 
         const char* Yb = reinterpret_cast<const char*>(&sm.Y[k + 1][0]);
         double* Yo = &sm.Y[k + 1][0];
@@ -234,10 +247,17 @@ __global__ void __launch_bounds__(64) k_skew(SkewArgs a) {
             f.dinv = __hiloint2double(int(c2.w), int(c2.z));
             f.rhs = sm.rhs[t & (PF - 1)][lane];
         };
+        auto group_wait = [&](unsigned q) {  // items and right-hand sides of group q are in
+            if (q < nq) {
+                const unsigned Q = gbase + q;
+                bar_wait(&sm.bar[Q % NG], (Q / NG) & 1);
+                bar_wait(&sm.rfull[Q % NG], (Q / NG) & 1);
+            }
+        };
         long long cyc[4] = {0, 0, 0, 0};
         long long c0 = clock64();
         auto tick = [&](int q) {
-            if (a.dbg & 16) {
+            if (TR && (a.dbg & 16)) {
                 const long long c1 = clock64();
                 cyc[q] += c1 - c0;
                 c0 = c1;
@@ -246,58 +266,62 @@ __global__ void __launch_bounds__(64) k_skew(SkewArgs a) {
         double res = 0.0, xprev = 0.0;
         Pre f;
         group_wait(0);
-        cp_wait<PF - 2>();  // rhs of step 0
         fetch(0, f);
-        for (int t = 0; t < NS; ++t) {
-            const int ix = t - P - D * k;  // the segment's stage-0 row at this step
-            tick(3);
-            rhs_issue(t + PF - 1);
-            group_wait(t + 1);
-            tick(0);
-            cp_wait<PF - 2>();  // rhs of step t+1 has landed
-            tick(1);
-            const double in0 = __shfl_down_sync(FULL, res, 1);  // partial from the next stage's lane
-            if (g0 > 0) {  // all lanes test (uniform branch; lane 0 publishes the ring use)
-                if (lane == 0) *reinterpret_cast<volatile int*>(&sm.cons_ix) = ix;
-                const int need = min(t - P + D, S);
-                // relaxed spin: shared-memory accesses of a warp are performed in order, and the
-                // bridge publishes with a release store
-                if (ld_vol_s(&sm.halo_ready) < need) {
-                    const long long w0 = clock64();
-                    while (ld_vol_s(&sm.halo_ready) < need) {
+        // steps are processed in groups of G (static ring positions)
+        for (int tb = 0; tb < NS; tb += G) {
+#pragma unroll
+            for (int u = 0; u < G; ++u) {
+                const int t = tb + u;
+                if (t >= NS) break;  // slots past the block's last group hold stale data
+                const int ix = t - P - D * k;  // the segment's stage-0 row at this step
+                tick(3);
+                if (u == G - 1) group_wait(unsigned(tb) / G + 1);  // for fetch(t + 1) below
+                tick(0);
+                const double in0 = __shfl_down_sync(FULL, res, 1);  // partial from the next stage's lane
+                if (g0 > 0) {  // all lanes test (uniform branch; lane 0 publishes the ring use)
+                    if (lane == 0) *reinterpret_cast<volatile int*>(&sm.cons_ix) = ix;
+                    const int need = min(t - P + D, S);
+                    // relaxed spin: shared-memory accesses of a warp are performed in order, and
+                    // the bridge publishes with a release store
+                    if (TR && a.trace && lane == 0 && need == 201) a.trace[(blk - 1) * 8 + 6] = gtimer();
+                    if (ld_vol_s(&sm.halo_ready) < need) {
+                        const long long w0 = clock64();
+                        while (ld_vol_s(&sm.halo_ready) < need) {
+                        }
+                        if (TR && a.trace && lane == 0) a.trace[blk * 8 + 2] += clock64() - w0;
                     }
-                    if (a.trace && lane == 0) a.trace[blk * 4 + 2] += clock64() - w0;
+                    if (TR && a.trace && lane == 0 && need == 201) a.trace[(blk - 1) * 8 + 7] = gtimer();
                 }
-            }
-            __syncwarp();
-            tick(2);
-            const double y0s = *reinterpret_cast<const double*>(Yb + f.o0);
-            const double y1 = *reinterpret_cast<const double*>(Yb + f.o1);
-            const double y2 = *reinterpret_cast<const double*>(Yb + f.o2);
-            const double in = role == 3 ? 0.0 : in0;
-            const double y0 = role == 0 ? (f.flag ? xprev : 0.0) : y0s;
-            const double r1 = in + f.w0 * y0;
-            res = (r1 + f.w1 * y1) + f.w2 * y2;
-            // stage-0 lanes: finalise (their w1, w2 are zero: r1 is the complete row sum)
-            const double x = K == kSkewL ? f.rhs - r1 : (f.rhs - r1) * f.dinv;
-            if (role == 0 && ix >= 0 && ix < rows) {
-                Yo[ix & (RY - 1)] = x;
-                st_relaxed(a.out + lo + ix, x);
-            }
-            xprev = x;
-            fetch(t + 1, f);  // static data of the next step (its group has landed)
-            if ((t + 1) % G == 0) {  // group (t+1)/G - 1 fully consumed: refill its slot
                 __syncwarp();
-                refill(unsigned(t + 1) / G - 1 + NG);
+                tick(2);
+                const double y0s = *reinterpret_cast<const double*>(Yb + f.o0);
+                const double y1 = *reinterpret_cast<const double*>(Yb + f.o1);
+                const double y2 = *reinterpret_cast<const double*>(Yb + f.o2);
+                const double in = role == 3 ? 0.0 : in0;
+                const double y0 = role == 0 ? (f.flag ? xprev : 0.0) : y0s;
+                const double r1 = in + f.w0 * y0;
+                res = (r1 + f.w1 * y1) + f.w2 * y2;
+                // stage-0 lanes: finalise (their w1, w2 are zero: r1 is the complete row sum)
+                const double x = K == kSkewL ? f.rhs - r1 : (f.rhs - r1) * f.dinv;
+                if (role == 0 && ix >= 0 && ix < rows) {
+                    Yo[ix & (RY - 1)] = x;
+                    st_relaxed(a.out + lo + ix, x);
+                    if (TR && a.trace && k == SPW - 1 && ix == 200) a.trace[blk * 8 + 4] = gtimer();
+                }
+                xprev = x;
+                fetch(t + 1, f);  // static data of the next step
             }
+            // group tb/G fully consumed: hand its rhs slots back, refill its item slots
+            __syncwarp();
+            const unsigned qd = unsigned(tb) / G;
+            if (lane == 0) bar_arrive(&sm.rempty[(gbase + qd) % NG]);
+            refill(qd + NG);
         }
-        cp_wait<0>();
-        if (a.trace && lane == 0) a.trace[blk * 4 + 1] = gtimer();
-        if ((a.dbg & 16) && a.trace && lane == 0 && blk == (a.dbg >> 8)) {
+        if (TR && a.trace && lane == 0) a.trace[blk * 8 + 1] = gtimer();
+        if (TR && (a.dbg & 16) && a.trace && lane == 0 && blk == (a.dbg >> 8)) {
             a.trace[2] = cyc[0] << 32 | cyc[1];  // (issue + group wait) | rhs wait
             a.trace[3] = cyc[2] << 32 | cyc[3];  // halo + syncwarp | compute + store
         }
-        gbase += nq;
     }
 }
 
@@ -492,8 +516,10 @@ void skew_sweep(const SkewOp& op, int* ticket, cudaStream_t st) {
     const int smem = int(sizeof(SkewSmem));
     static bool attr = false;
     if (!attr) {
-        PMG_CUDA(cudaFuncSetAttribute(k_skew<kSkewL>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        PMG_CUDA(cudaFuncSetAttribute(k_skew<kSkewU>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        PMG_CUDA(cudaFuncSetAttribute(k_skew<kSkewL, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        PMG_CUDA(cudaFuncSetAttribute(k_skew<kSkewU, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        PMG_CUDA(cudaFuncSetAttribute(k_skew<kSkewL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        PMG_CUDA(cudaFuncSetAttribute(k_skew<kSkewU, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         attr = true;
     }
     static int dbg = -1;
@@ -505,14 +531,24 @@ void skew_sweep(const SkewOp& op, int* ticket, cudaStream_t st) {
     if (g_skew_trace_on) {  // one-shot trace of the next sweep (diagnostics)
         g_skew_trace_on = false;
         cudaFree(g_skew_trace);
-        PMG_CUDA(cudaMalloc(&g_skew_trace, sizeof(unsigned long long) * 4 * nblk));
-        PMG_CUDA(cudaMemsetAsync(g_skew_trace, 0, sizeof(unsigned long long) * 4 * nblk, st));
+        PMG_CUDA(cudaMalloc(&g_skew_trace, sizeof(unsigned long long) * 8 * nblk));
+        PMG_CUDA(cudaMemsetAsync(g_skew_trace, 0, sizeof(unsigned long long) * 8 * nblk, st));
         g_skew_trace_n = nblk;
         a.trace = g_skew_trace;
     }
-    const int grid = std::min(nblk, nsm);
-    if (op.kind == kSkewL) k_skew<kSkewL><<<grid, 64, smem, st>>>(a);
-    else k_skew<kSkewU><<<grid, 64, smem, st>>>(a);
+    static int grid_cap = -1;  // tests: fewer CTAs than blocks (CTAs then loop over blocks)
+    if (grid_cap < 0) {
+        const char* e = getenv("PMG_SKEW_GRID");
+        grid_cap = e ? std::max(1, atoi(e)) : 0;
+    }
+    const int grid = std::min(std::min(nblk, nsm), grid_cap > 0 ? grid_cap : nsm);
+    if (a.trace) {
+        if (op.kind == kSkewL) k_skew<kSkewL, true><<<grid, 96, smem, st>>>(a);
+        else k_skew<kSkewU, true><<<grid, 96, smem, st>>>(a);
+    } else {
+        if (op.kind == kSkewL) k_skew<kSkewL, false><<<grid, 96, smem, st>>>(a);
+        else k_skew<kSkewU, false><<<grid, 96, smem, st>>>(a);
+    }
     PMG_LAUNCH_CHECK();
     if (op.kind == kSkewU) {
         k_skew_upd<<<ceil_div(n, 256), 256, 0, st>>>(op.out, op.upd, n);

@@ -135,11 +135,12 @@ def test_solve_config3(sweep_path):
     assert rep.converged
 
 
-@pytest.mark.parametrize("h_exp", [5, 6, 8])
+@pytest.mark.parametrize("h_exp", [4, 5, 6, 8])
 @pytest.mark.parametrize("geometry", ["square", "annulus"])
 def test_skew_sweeps_p1(h_exp, geometry, monkeypatch):
-    """The skewed-warp sweeps (skew.cu) on p=1 factors: one warp block (h=2^-5: 33 segments
-    -> 2 blocks), several blocks with halo hand-offs (2^-6, 2^-8), bitwise against the oracle."""
+    """The skewed-warp sweeps (skew.cu) on p=1 factors: one 8-segment warp block (h=2^-4:
+    17 segments -> 3 blocks), many blocks with halo hand-offs (2^-5 .. 2^-8), bitwise against
+    the oracle."""
     monkeypatch.delenv("PMG_SKEW", raising=False)
     monkeypatch.delenv("PMG_FORCE_LEVELSCHED", raising=False)
     spec = P.make_spec(geometry=geometry, rhs="one", degrees=(2, 1), h_exp=h_exp)
@@ -152,3 +153,24 @@ def test_skew_sweeps_p1(h_exp, geometry, monkeypatch):
     for _ in range(3):
         r = rng.uniform(-1, 1, A.nrows)
         assert_bitwise(pmg.ilut_apply(Fg, r), Fo.apply(r), "skew ilut_apply")
+
+
+def test_skew_sweeps_cta_loops():
+    """Fewer CTAs than warp blocks (PMG_SKEW_GRID, read once per process): CTAs claim blocks in
+    order and re-arm their barriers per block.  Run in a subprocess so the cap stays local."""
+    import os, subprocess, sys
+    code = (
+        "import numpy as np, sys; sys.path.insert(0, '.');"
+        "from oracle import oracle as O; from paper_1901_01685_b200 import pmg, problems as P;"
+        "A = P.build(P.make_spec(geometry='annulus', rhs='one', degrees=(2, 1), h_exp=7)).hlevels[0].A;"
+        "F = pmg.ilut_factorize(A, 1e-12, 1.0, 'none'); assert F.stats()['sweep'] == 'skew';"
+        "Fo = O.ilut_factorize(A, 1e-12, 1.0, O.ORDER_NONE);"
+        "r = np.random.default_rng(3).uniform(-1, 1, A.nrows);"
+        "e, eo = pmg.ilut_apply(F, r), Fo.apply(r);"
+        "assert (e.view(np.uint64) == eo.view(np.uint64)).all(), 'mismatch'"
+    )
+    env = dict(os.environ, PMG_SKEW_GRID="3")
+    env.pop("PMG_SKEW", None)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
