@@ -329,20 +329,21 @@ int make_factor(pmg_csr_s* A, double tau, double fillfactor, int ordering, pmg_f
     // short rows (p=1 factors): the per-segment lag is dominated by the finisher batch
     F->bs = std::max(F->max_row_L, F->max_row_U) <= 16 ? 8 : 32;
     if (const char* e = getenv("PMG_CHAIN_BS")) F->bs = atoi(e);
-    // short rows and reach (the p=1 h-levels): skewed-warp sweeps (skew.cu); PMG_SKEW=0 keeps
-    // the chained-segment kernel for every factor
+    // tensor-grid orderings: skewed-warp sweeps (skew.cu); PMG_SKEW=0 keeps the
+    // chained-segment kernel for every factor
     const char* sk = getenv("PMG_SKEW");
-    if (F->seg > 0 && !F->perm && !(sk && sk[0] == '0') && F->max_row_L <= kSkewSlots &&
-        F->max_row_U - 1 <= kSkewSlots) {
-        const bool okL = skew_plan(F->Ls, nullptr, F->seg, kSkewL, F->planL, st);
-        const bool okU = okL && skew_plan(F->Us, F->Udiag, F->seg, kSkewU, F->planU, st);
+    if (F->seg > 0 && !F->perm && !(sk && sk[0] == '0')) {
+        const bool okL = skew_plan(F->Ls, nullptr, F->seg, kSkewL, F->max_row_L, F->planL, st);
+        const bool okU = okL && skew_plan(F->Us, F->Udiag, F->seg, kSkewU, F->max_row_U - 1, F->planU, st);
         F->skew = okL && okU;
         if (!F->skew) {
             skew_plan_free(F->planL);
             skew_plan_free(F->planU);
         }
         if (getenv("PMG_VERBOSE"))
-            fprintf(stderr, "[pmg] factor n=%d skew %d D %d/%d\n", F->n, int(F->skew), F->planL.D, F->planU.D);
+            fprintf(stderr, "[pmg] factor n=%d skew %d NRxC %dx%d D %d/%d dm %d/%d ring %d/%d\n", F->n, int(F->skew),
+                    F->planL.nr, F->planL.c, F->planL.D, F->planU.D, F->planL.dm, F->planU.dm, F->planL.ry,
+                    F->planU.ry);
     }
     *out = F.release();
     return PMG_OK;
@@ -983,8 +984,8 @@ int pmg_factor_stats(pmg_factor F, int64_t* nnz_L, int64_t* nnz_U, int32_t* leve
 int pmg_factor_sweep_info(pmg_factor F, int32_t* kind, int32_t* seg, int32_t* skew_D_L, int32_t* skew_D_U) {
     if (kind) *kind = F->skew ? PMG_SWEEP_SKEW : F->seg > 0 ? PMG_SWEEP_CHAIN : PMG_SWEEP_LEVELS;
     if (seg) *seg = F->seg;
-    if (skew_D_L) *skew_D_L = F->skew ? F->planL.D : 0;
-    if (skew_D_U) *skew_D_U = F->skew ? F->planU.D : 0;
+    if (skew_D_L) *skew_D_L = F->skew ? F->planL.lead : 0;
+    if (skew_D_U) *skew_D_U = F->skew ? F->planU.lead : 0;
     return PMG_OK;
 }
 

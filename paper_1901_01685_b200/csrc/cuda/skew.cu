@@ -1,29 +1,30 @@
-// Skewed-warp wavefront sweeps for factors with short rows and short reach (the p=1 h-levels).
+// Skewed-warp wavefront sweeps for sparse triangular solves on tensor-grid orderings.
 //
 // v-order and segments as in chain.cu (segment = one grid row of S rows; L: ascending rows,
-// U: descending rows).  A warp owns a block of SPW = 8 consecutive segments; four lanes
-// serve each segment, one per pipeline stage.  At step t the stage-s lane of segment k works
-// on row ix + s, ix = t - P - k*D: it adds its stage's (<= 3) terms, in the oracle's
-// ascending order, to the partial sum the stage-(s+1) lane handed over (shuffle) at the end
-// of step t-1; the stage-0 lane adds the v-1 term (its own previous output, a register) and
-// finalises the row.  Every value a term needs is already on chip:
-//   * values of the row's own segment: the segment's ring in shared memory;
-//   * values one segment back: segment k-1's ring, written >= 1 step earlier because the lane
-//     skew D covers the forward reach (chosen per factor at plan time);
-//   * segment 0's values one segment back come from the previous block (another CTA) through
-//     global memory: a bridge warp polls them (NaN-sentinel protocol), copies them into the
-//     halo ring and publishes how many are in.
+// U: descending rows).  A row's terms (its entries in ascending v-column) are assigned to
+// pipeline stages at plan time: stage 0 is the v-1 term, stages 1..P hold C terms each,
+// counted back from the end, so stage s is summed s steps before the row is finalised.
+// NR = P+1 lanes serve one segment, one per stage; a warp owns SPW = 32/NR consecutive
+// segments (a "block") and at step t the stage-s lane of segment k works on row
+// ix + s, ix = t - P - k*D.  It adds its stage's terms, in the oracle's ascending order, to
+// the partial sum the stage-(s+1) lane handed over (shuffle) at the end of step t-1; the
+// stage-0 lane adds the v-1 term (its own previous output, a register) and finalises the row.
+// Every value a term needs is already on chip:
+//   * own segment: the segment's ring in shared memory;
+//   * d segments back inside the block: that segment's ring, written >= 1 step earlier because
+//     the lane skew D covers the forward reach (D >= (stage + 1 + jx - ix) / d per term);
+//   * d segments back beyond the block: halo rings, filled from global memory by a bridge warp
+//     that polls the previous block's last DM segments (NaN-sentinel protocol).
 // The per-step static data (coefficients and shared-memory offsets of every lane's terms) is
 // stored step-major per block and moved by bulk copies (cp.async.bulk + mbarrier) into a ring;
-// the right-hand side is gathered per step with cp.async.  A sweep costs about
-// nseg * D steps; a step is one shuffle + three dependent adds on its critical path.
+// a stager warp gathers the right-hand sides.  A sweep costs about nseg * D steps; a step is a
+// shuffle plus C dependent adds on its critical path.
 //
-// Compared with chain.cu (one CTA per segment, cross-segment hops through L2 for every
-// segment) only every 8th segment boundary crosses the memory system here, which is what the
-// p=1 factors (9 entries per row, reach ~8 rows) need: their chained sweeps were bound by the
-// per-segment hop latency, not by work.
+// Layouts per factor (chosen by skew_plan from the longest row): NR x C = 4 x 3 (p = 1,
+// <= 10 terms), 8 x 4 (<= 29), 16 x 4 (<= 61), 32 x 3 (<= 94), 32 x 4 (<= 125).
 #include <climits>
 #include <cstdlib>
+#include <vector>
 
 #include "skew.cuh"
 
@@ -31,50 +32,50 @@ namespace pmg {
 
 namespace {
 
-constexpr int SPW = 8;        // segments per warp block
-constexpr int NR = kSkewP + 1;  // lanes per segment (one per stage)
-constexpr int RY = 64;        // per-segment ring of recent outputs
-constexpr int RYS = RY + 1;   // + a zero cell (padding terms point at it)
 constexpr int G = 16;         // steps per bulk copy
 constexpr int NG = 4;         // bulk-copy groups in the ring
 constexpr int PF = G * NG;    // steps staged
 constexpr int ICH = 3;        // 16-B chunks per (step, lane) item
 constexpr int STEP_BYTES = ICH * 32 * 16;
-constexpr int P = kSkewP, C = kSkewC;
+constexpr int MAXD = 8;       // segments back a term may reach
 constexpr unsigned FULL = 0xffffffffu;
-static_assert(SPW * NR == 32, "one warp per block");
+constexpr int NT = 96;        // sweep warp, bridge warp, stager warp
 
 // per (step, lane) item: the lane's stage data for the row it works on at that step
-//   stage s >= 1: w[0..2], o[0..2] = coefficients / byte offsets of the stage's terms
-//   stage 0     : w[0] = coefficient of the v-1 term, flag = has0, dinv
+//   stage s >= 1: w[0..3], o[0..3] = coefficients / byte offsets of the stage's terms
+//   stage 0     : w[0] = coefficient of the v-1 term, w[1] = 1/diagonal (U), o[0] = 8 if
+//                 the row has a v-1 term else 0, o[1..3] = zero cell
 struct __align__(16) SkewItem {
-    double w[3];
-    int32_t o[3];
-    int32_t flag;
-    double dinv;
+    double w[4];
+    int32_t o[4];
 };
 static_assert(sizeof(SkewItem) == ICH * 16, "SkewItem layout");
 
 struct SkewSmem {
     uint4 item[PF][ICH][32];  // [step slot][16-B chunk][lane]: conflict-free 128-bit reads
     double rhs[PF][32];
-    double Y[SPW + 1][RYS];   // row 0: halo (previous block's last segment); row k+1: segment k
     unsigned long long bar[NG];     // items of a group have landed (bulk copy)
     unsigned long long rfull[NG];   // right-hand sides of a group are in (stager warp)
     unsigned long long rempty[NG];  // a group's slots were consumed (sweep warp)
-    int halo_ready;           // halo values [0, halo_ready) are in
+    int halo_ready;           // segment 0 may work on rows < halo_ready + 1 (all halo values it needs are in)
     int cons_ix;              // segment 0's current row (halo ring reuse)
     int blk;
+    int pad;
+    // followed by double Y[DM + SPW][RY + 1]: rows 0..DM-1 halo (segment g0-DM .. g0-1),
+    // row DM + k: segment k of the block; cell RY of every row is a zero
 };
 
 struct SkewArgs {
     const uint4* item;
     const double* rhs;
     double* out;
-    int32_t n, seg, nseg, D, b1, ns_full;
+    const int32_t* Db;        // [nblk] lane skew of the block
+    const int64_t* off;       // [nblk+1] first step of the block in the item stream
+    const int32_t* R;         // [nblk][MAXD] lead (rows) a halo segment needs over segment 0
+    const int32_t* W;         // [nblk][MAXD] how far behind segment 0 a halo value is still read
+    int32_t n, seg, nseg, dm, ry;
     int* ticket;
-    unsigned long long* trace;  // optional: per block [claim, end, halo spins, bridge polls]
-    int dbg;                    // timing experiments only (PMG_SKEW_DBG bits)
+    unsigned long long* trace;  // optional: per block [claim, end, halo wait cycles, bridge polls, ...]
 };
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
@@ -89,14 +90,6 @@ __device__ __forceinline__ int vcol(int c, int n) {
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void cp_async8_z(void* dst, const void* src, int bytes) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 __device__ __forceinline__ void bar_init(unsigned long long* b) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(b)) : "memory");
@@ -119,29 +112,26 @@ __device__ __forceinline__ void bar_wait(unsigned long long* b, unsigned parity)
         "r"(parity)
         : "memory");
 }
-__device__ __forceinline__ int ld_acq_cta(const int* p) {
-    int v;
-    asm volatile("ld.acquire.cta.shared.b32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
-    return v;
-}
 __device__ __forceinline__ void st_rel_cta(int* p, int v) {
     asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
 }
 __device__ __forceinline__ int ld_vol_s(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
 
-template <int K, bool TR>
-__global__ void __launch_bounds__(96) k_skew(SkewArgs a) {
+template <int K, int NR, int C, bool TR>
+__global__ void __launch_bounds__(NT) k_skew(SkewArgs a) {
+    constexpr int SPW = 32 / NR, P = NR - 1;
     extern __shared__ __align__(128) unsigned char skew_smem[];
     SkewSmem& sm = *reinterpret_cast<SkewSmem*>(skew_smem);
+    const int DM = a.dm, RY = a.ry, RYS = a.ry + 1;
+    double* Ybase = reinterpret_cast<double*>(skew_smem + sizeof(SkewSmem));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int n = a.n, S = a.seg, D = a.D;
-    constexpr unsigned gbase = 0;  // barriers are re-initialised per block: group q <-> slot q % NG
+    const int n = a.n, S = a.seg;
 
     for (;;) {
         __syncthreads();
         if (threadIdx.x == 0) {
             sm.blk = atomicAdd(a.ticket, 1);
-            sm.halo_ready = 0;
+            sm.halo_ready = INT_MIN / 2;
             sm.cons_ix = -P;
             // every copy / arrival of the previous block has been waited for or has completed
             for (int q = 0; q < NG; ++q) {
@@ -151,31 +141,34 @@ __global__ void __launch_bounds__(96) k_skew(SkewArgs a) {
             }
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
-        for (int q = threadIdx.x; q < (SPW + 1) * RYS; q += 96) (&sm.Y[0][0])[q] = 0.0;
+        for (int q = threadIdx.x; q < (DM + SPW) * RYS; q += NT) Ybase[q] = 0.0;
         __syncthreads();
         const int blk = sm.blk;
         const int g0 = blk * SPW;
         if (g0 >= a.nseg) break;
         if (TR && a.trace && threadIdx.x == 0) a.trace[blk * 8 + 0] = gtimer();
-        const int kmax = min(SPW - 1, a.nseg - 1 - g0);
-        const int T = S + kmax * D;
-        const int NS = T + P;                       // steps of this block (t = tau + P)
+        const int D = a.Db[blk];
+        const int NS = int(a.off[blk + 1] - a.off[blk]);  // steps of this block (t = tau + P)
         const unsigned nq = (NS + G - 1) / G;       // bulk-copy groups of this block
 
         if (warp == 2) {
             // ---------------------------------------------------------------- stager
             // right-hand sides of the stage-0 rows, group by group, into the rhs ring
             for (unsigned q = 0; q < nq; ++q) {
-                const unsigned Q = gbase + q, slot = Q % NG, use = Q / NG;
+                const unsigned slot = q % NG, use = q / NG;
                 if (use > 0) bar_wait(&sm.rempty[slot], (use - 1) & 1);
 #pragma unroll
                 for (int e0 = 0; e0 < G * SPW; e0 += 32) {
-                    const int e = e0 + lane, st = int(q) * G + e / SPW, kk = e % SPW;
-                    const int gg = g0 + kk, ix = st - P - D * kk;
-                    const int64_t lo2 = int64_t(gg) * S;
-                    const bool in = gg < a.nseg && ix >= 0 && ix < S && lo2 + ix < n;
-                    const int64_t v = lo2 + ix;
-                    sm.rhs[slot * G + e / SPW][kk * NR] = in ? a.rhs[K == kSkewL ? v : int64_t(n) - 1 - v] : 0.0;
+                    const int e = e0 + lane;
+                    if (G * SPW >= 32 || e < G * SPW) {
+                        const int st = int(q) * G + e / SPW, kk = e % SPW;
+                        const int gg = g0 + kk, ix = st - P - D * kk;
+                        const int64_t lo2 = int64_t(gg) * S;
+                        const bool in = gg < a.nseg && ix >= 0 && ix < S && lo2 + ix < n;
+                        const int64_t v = lo2 + ix;
+                        sm.rhs[slot * G + e / SPW][kk * NR] =
+                            in ? a.rhs[K == kSkewL ? v : int64_t(n) - 1 - v] : 0.0;
+                    }
                 }
                 __syncwarp();
                 if (lane == 0) bar_arrive(&sm.rfull[slot]);
@@ -184,24 +177,48 @@ __global__ void __launch_bounds__(96) k_skew(SkewArgs a) {
         }
         if (warp == 1) {
             // ---------------------------------------------------------------- bridge
-            // previous block's last segment -> halo ring, in order, as its values appear
+            // the previous block's last DM segments -> halo rings, in order, as values appear.
+            // halo_ready = h publishes [0, h + (delta-1)*D) of segment g0-delta for every delta.
             if (g0 > 0) {
-                const double* src = a.out + int64_t(g0 - 1) * S;
-                int j0 = 0;
+                int f[MAXD], Rq[MAXD], Wq[MAXD];
+#pragma unroll
+                for (int d = 0; d < MAXD; ++d) {
+                    Rq[d] = d < DM ? a.R[blk * MAXD + d] : INT_MIN;
+                    Wq[d] = d < DM ? a.W[blk * MAXD + d] : 0;
+                    f[d] = (Rq[d] > INT_MIN / 2 && g0 - 1 - d >= 0) ? 0 : S;  // halo rows nobody reads: done
+                }
+                int pub = INT_MIN / 2;
                 unsigned ns = 16;
-                while (j0 < S) {
-                    const int cap = ld_vol_s(&sm.cons_ix) - a.b1 + RY - j0;  // ring slots free
-                    const int j = j0 + lane;
-                    double v = sentinel();
-                    if (lane < cap && j < S) v = ld_relaxed_nb(src + j);
-                    const unsigned ok = __ballot_sync(FULL, !is_sentinel(v));
-                    const int cnt = ok == FULL ? 32 : __ffs(~ok) - 1;
-                    if (lane < cnt) sm.Y[0][j & (RY - 1)] = v;
-                    if (TR && a.trace && lane < cnt && j == 200) a.trace[(blk - 1) * 8 + 5] = gtimer();
+                while (pub < INT_MAX / 2) {
+                    const int cons = ld_vol_s(&sm.cons_ix);
+                    double v[MAXD];
+#pragma unroll
+                    for (int d = 0; d < MAXD; ++d) {  // halo distance delta = d + 1: all polls in flight at once
+                        v[d] = sentinel();
+                        const int cap = cons - Wq[d] + RY - f[d];  // ring slots free
+                        const int j = f[d] + lane;
+                        if (d < DM && f[d] < S && lane < cap && j < S)
+                            v[d] = ld_relaxed_nb(a.out + int64_t(g0 - 1 - d) * S + j);
+                    }
+                    bool moved = false;
+                    int h = INT_MAX / 2;
+#pragma unroll
+                    for (int d = 0; d < MAXD; ++d) {
+                        if (d < DM && f[d] < S) {
+                            const unsigned ok = __ballot_sync(FULL, !is_sentinel(v[d]));
+                            const int cnt = ok == FULL ? 32 : __ffs(~ok) - 1;
+                            if (lane < cnt) Ybase[(DM - 1 - d) * RYS + ((f[d] + lane) & (RY - 1))] = v[d];
+                            f[d] += cnt;
+                            moved = moved || cnt > 0;
+                            if (f[d] < S) h = min(h, f[d] - Rq[d]);
+                        }
+                    }
                     __syncwarp();
-                    if (cnt > 0) {
-                        if (lane == 0) st_rel_cta(&sm.halo_ready, j0 + cnt);
-                        j0 += cnt;
+                    if (h > pub) {
+                        if (lane == 0) st_rel_cta(&sm.halo_ready, h);
+                        pub = h;
+                    }
+                    if (moved) {
                         ns = 16;
                     } else {
                         __nanosleep(ns);
@@ -214,220 +231,239 @@ __global__ void __launch_bounds__(96) k_skew(SkewArgs a) {
         }
 
         // -------------------------------------------------------------------- sweep warp
-        const int k = lane >> 2, role = lane & 3;   // segment in the block, stage of the lane
+        const int k = lane / NR, role = lane % NR;  // segment in the block, stage of the lane
         const int g = g0 + k;
         const int64_t lo = int64_t(g) * S;
         const int rows = g < a.nseg ? int(min(int64_t(S), int64_t(n) - lo)) : 0;
-        const unsigned char* bsrc = reinterpret_cast<const unsigned char*>(a.item) + int64_t(blk) * a.ns_full * STEP_BYTES;
+        const unsigned char* bsrc =
+            reinterpret_cast<const unsigned char*>(a.item) + a.off[blk] * STEP_BYTES;
         auto refill = [&](unsigned q) {  // group q of this block's steps -> its ring slot
-            if (lane == 0 && q * G < unsigned(NS)) {
-                const unsigned slot = (gbase + q) % NG;
+            if (lane == 0 && q < nq) {
+                const unsigned slot = q % NG;
                 const unsigned bytes = min(G, NS - int(q * G)) * STEP_BYTES;
                 bulk_load(&sm.item[slot * G][0][0], bsrc + int64_t(q) * G * STEP_BYTES, bytes, &sm.bar[slot]);
             }
         };
         for (unsigned q = 0; q < NG; ++q) refill(q);
 
-        const char* Yb = reinterpret_cast<const char*>(&sm.Y[k + 1][0]);
-        double* Yo = &sm.Y[k + 1][0];
+        const char* Yb = reinterpret_cast<const char*>(Ybase + (DM + k) * RYS);
+        double* Yo = Ybase + (DM + k) * RYS;
         struct Pre {
-            double w0, w1, w2, dinv, rhs;
-            int o0, o1, o2, flag;
+            double w[4], rhs;
+            int o[4];
         };
         auto fetch = [&](int t, Pre& f) {  // static data of step t from the ring
             const uint4* it = &sm.item[t & (PF - 1)][0][lane];
             const uint4 c0 = it[0], c1 = it[32], c2 = it[64];
-            f.w0 = __hiloint2double(int(c0.y), int(c0.x));
-            f.w1 = __hiloint2double(int(c0.w), int(c0.z));
-            f.w2 = __hiloint2double(int(c1.y), int(c1.x));
-            f.o0 = int(c1.z);
-            f.o1 = int(c1.w);
-            f.o2 = int(c2.x);
-            f.flag = int(c2.y);
-            f.dinv = __hiloint2double(int(c2.w), int(c2.z));
+            f.w[0] = __hiloint2double(int(c0.y), int(c0.x));
+            f.w[1] = __hiloint2double(int(c0.w), int(c0.z));
+            f.w[2] = __hiloint2double(int(c1.y), int(c1.x));
+            f.w[3] = __hiloint2double(int(c1.w), int(c1.z));
+            f.o[0] = int(c2.x);
+            f.o[1] = int(c2.y);
+            f.o[2] = int(c2.z);
+            f.o[3] = int(c2.w);
             f.rhs = sm.rhs[t & (PF - 1)][lane];
         };
         auto group_wait = [&](unsigned q) {  // items and right-hand sides of group q are in
             if (q < nq) {
-                const unsigned Q = gbase + q;
-                bar_wait(&sm.bar[Q % NG], (Q / NG) & 1);
-                bar_wait(&sm.rfull[Q % NG], (Q / NG) & 1);
-            }
-        };
-        long long cyc[4] = {0, 0, 0, 0};
-        long long c0 = clock64();
-        auto tick = [&](int q) {
-            if (TR && (a.dbg & 16)) {
-                const long long c1 = clock64();
-                cyc[q] += c1 - c0;
-                c0 = c1;
+                bar_wait(&sm.bar[q % NG], (q / NG) & 1);
+                bar_wait(&sm.rfull[q % NG], (q / NG) & 1);
             }
         };
         double res = 0.0, xprev = 0.0;
+        int hr = INT_MIN / 2;  // last seen halo_ready
         Pre f;
         group_wait(0);
         fetch(0, f);
-        // steps are processed in groups of G (static ring positions)
         for (int tb = 0; tb < NS; tb += G) {
 #pragma unroll
             for (int u = 0; u < G; ++u) {
                 const int t = tb + u;
                 if (t >= NS) break;  // slots past the block's last group hold stale data
                 const int ix = t - P - D * k;  // the segment's stage-0 row at this step
-                tick(3);
                 if (u == G - 1) group_wait(unsigned(tb) / G + 1);  // for fetch(t + 1) below
-                tick(0);
                 const double in0 = __shfl_down_sync(FULL, res, 1);  // partial from the next stage's lane
                 if (g0 > 0) {  // all lanes test (uniform branch; lane 0 publishes the ring use)
-                    if (lane == 0) *reinterpret_cast<volatile int*>(&sm.cons_ix) = ix;
-                    const int need = min(t - P + D, S);
-                    // relaxed spin: shared-memory accesses of a warp are performed in order, and
-                    // the bridge publishes with a release store
-                    if (TR && a.trace && lane == 0 && need == 201) a.trace[(blk - 1) * 8 + 6] = gtimer();
-                    if (ld_vol_s(&sm.halo_ready) < need) {
+                    if (lane == 0) *reinterpret_cast<volatile int*>(&sm.cons_ix) = t - P;
+                    // hr was loaded one step ago, so the test is off the critical path unless
+                    // segment 0 runs right behind the halo; relaxed loads: shared-memory
+                    // accesses of a warp are performed in order, the bridge publishes with a
+                    // release store
+                    if (hr < t - P) {
                         const long long w0 = clock64();
-                        while (ld_vol_s(&sm.halo_ready) < need) {
-                        }
+                        do {
+                            hr = ld_vol_s(&sm.halo_ready);
+                        } while (hr < t - P);
                         if (TR && a.trace && lane == 0) a.trace[blk * 8 + 2] += clock64() - w0;
                     }
-                    if (TR && a.trace && lane == 0 && need == 201) a.trace[(blk - 1) * 8 + 7] = gtimer();
                 }
                 __syncwarp();
-                tick(2);
-                const double y0s = *reinterpret_cast<const double*>(Yb + f.o0);
-                const double y1 = *reinterpret_cast<const double*>(Yb + f.o1);
-                const double y2 = *reinterpret_cast<const double*>(Yb + f.o2);
-                const double in = role == 3 ? 0.0 : in0;
-                const double y0 = role == 0 ? (f.flag ? xprev : 0.0) : y0s;
-                const double r1 = in + f.w0 * y0;
-                res = (r1 + f.w1 * y1) + f.w2 * y2;
-                // stage-0 lanes: finalise (their w1, w2 are zero: r1 is the complete row sum)
-                const double x = K == kSkewL ? f.rhs - r1 : (f.rhs - r1) * f.dinv;
+                double y[C];
+#pragma unroll
+                for (int q = 0; q < C; ++q) y[q] = *reinterpret_cast<const double*>(Yb + f.o[q]);
+                const double in = role == NR - 1 ? 0.0 : in0;
+                if (role == 0) y[0] = f.o[0] ? xprev : 0.0;
+                const double r1 = in + f.w[0] * y[0];
+                double r = r1;
+#pragma unroll
+                for (int q = 1; q < C; ++q) r = r + f.w[q] * y[q];
+                res = r;
+                // stage-0 lanes: finalise (r1 is their complete row sum, w[1] their 1/diagonal)
+                const double x = K == kSkewL ? f.rhs - r1 : (f.rhs - r1) * f.w[1];
                 if (role == 0 && ix >= 0 && ix < rows) {
                     Yo[ix & (RY - 1)] = x;
                     st_relaxed(a.out + lo + ix, x);
-                    if (TR && a.trace && k == SPW - 1 && ix == 200) a.trace[blk * 8 + 4] = gtimer();
                 }
                 xprev = x;
+                if (g0 > 0) hr = ld_vol_s(&sm.halo_ready);  // for the next step's test
                 fetch(t + 1, f);  // static data of the next step
             }
             // group tb/G fully consumed: hand its rhs slots back, refill its item slots
             __syncwarp();
             const unsigned qd = unsigned(tb) / G;
-            if (lane == 0) bar_arrive(&sm.rempty[(gbase + qd) % NG]);
+            if (lane == 0) bar_arrive(&sm.rempty[qd % NG]);
             refill(qd + NG);
         }
         if (TR && a.trace && lane == 0) a.trace[blk * 8 + 1] = gtimer();
-        if (TR && (a.dbg & 16) && a.trace && lane == 0 && blk == (a.dbg >> 8)) {
-            a.trace[2] = cyc[0] << 32 | cyc[1];  // (issue + group wait) | rhs wait
-            a.trace[3] = cyc[2] << 32 | cyc[3];  // halo + syncwarp | compute + store
-        }
     }
 }
 
-// The record of row v (v-order) of factor S: stage assignment and shared-memory offsets.
-// flags: bit 0 = does not fit.  dreq / back1 / back0 as documented in skew_plan.
+// The terms of row v (v-order) of factor S, ascending v-column: count and accessors.
 template <int K>
-__device__ void skew_record(const Sell& S, const double* dinv, int32_t seg, int32_t v, SkewRec& r, int& fail,
-                            int& dreq, int& back1, int& back0) {
-    const int n = S.n, g = v / seg, ix = v - g * seg;
-    const int64_t base = S.off[v >> 5];
-    const int li = v & 31;
-    const int len = S.len[v];
-#pragma unroll
-    for (int s = 0; s < kSkewSlots; ++s) {
-        r.coef[s] = 0.0;
-        if (s < kSkewSlots - 1) r.off[s] = RY * 8;  // the lane's zero cell
-    }
-    r.has0 = 0;
-    r.dinv = K == kSkewU ? dinv[v] : 1.0;
-    fail = len > kSkewSlots;
-    dreq = 1;
-    back1 = back0 = INT_MIN;
-    int q = len - 1;
-    auto col_at = [&](int k) { return vcol<K>(S.col[base + (k >> 2) * 128 + li * 4 + (k & 3)], n); };
-    auto val_at = [&](int k) { return S.val[base + (k >> 1) * 64 + li * 2 + (k & 1)]; };
-    if (!fail && q >= 0 && col_at(q) == v - 1 && ix > 0) {
-        r.coef[P * C] = val_at(q);
-        r.has0 = 1;
-        --q;
-    }
-    int st = 1, used = 0, prev = INT_MAX;
-    for (; !fail && q >= 0; --q) {
-        const int c = col_at(q);
-        if (c >= prev || c >= v) fail = 1;  // terms must be strictly ascending and below v
+struct RowView {
+    const Sell& S;
+    int v, n, len;
+    int64_t base;
+    int li;
+    __device__ RowView(const Sell& s, int v_) : S(s), v(v_), n(s.n), len(s.len[v_]), base(s.off[v_ >> 5]), li(v_ & 31) {}
+    __device__ int col(int k) const { return vcol<K>(S.col[base + (k >> 2) * 128 + li * 4 + (k & 3)], n); }
+    __device__ double val(int k) const { return S.val[base + (k >> 1) * 64 + li * 2 + (k & 1)]; }
+};
+
+// Walk the terms of row v with their stages: f(stage, d, jx) for every term before the v-1
+// term; returns false if a term does not fit the layout (more than P stages, own value not
+// final by its stage, not ascending, more than MAXD segments back).
+template <int K, class F>
+__device__ bool for_terms(const Sell& S, int32_t seg, int v, int NR, int C, F&& f) {
+    RowView<K> r(S, v);
+    const int g = v / seg, ix = v - g * seg, P = NR - 1;
+    int q = r.len - 1;
+    if (q >= 0 && r.col(q) == v - 1 && ix > 0) --q;  // stage 0: the v-1 term
+    int prev = INT_MAX;
+    bool ok = true;
+    for (int b = 0; q >= 0; --q, ++b) {
+        const int c = r.col(q);
+        if (c >= prev || c >= v) ok = false;  // terms must be strictly ascending and below v
         prev = c;
-        if (used == C) {
-            ++st;
-            used = 0;
-        }
-        if (st > P) {
-            fail = 1;
-            break;
-        }
+        const int st = 1 + b / C;
+        if (st > P) return false;
         const int gc = c / seg, jx = c - gc * seg, d = g - gc;
-        if (d == 0) {
-            if (st > ix - jx - 1) fail = 1;  // own value not final by the stage's step
-            back0 = max(back0, ix - jx - st);
-        } else if (d == 1) {
-            dreq = max(dreq, st + 1 + jx - ix);
-            back1 = max(back1, ix - jx - st);
-        } else {
-            fail = 1;
-        }
-        const int slot = (P - st) * C + (C - 1 - used);
-        r.coef[slot] = val_at(q);
-        r.off[slot] = (-d * RYS + (jx & (RY - 1))) * 8;
-        ++used;
+        if (d == 0 && st > ix - jx - 1) ok = false;  // own value not final by the stage's step
+        if (d > MAXD) return false;
+        f(st, d, jx, ix);
     }
+    return ok;
 }
 
-// pass 1: out[0] = required D, out[1] = failure flag, out[2] = max (ix - jx - stage) over
-// terms one segment back, out[3] = same over the own segment
+// pass 1a: per block, the lane skew D_b covering every term inside the block; global failure,
+// own-segment back reach and segments-back reach.  out[0] fail, out[1] back0, out[2] dmax
 template <int K>
-__global__ void k_skew_req(Sell S, const double* __restrict__ dinv, int32_t seg, int* out) {
+__global__ void k_skew_req(Sell S, int32_t seg, int NR, int C, int32_t* Db, int* out) {
     const int32_t v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= S.n) return;
-    SkewRec r;
-    int fail, dreq, back1, back0;
-    skew_record<K>(S, dinv, seg, v, r, fail, dreq, back1, back0);
-    atomicMax(out + 0, dreq);
-    if (fail) atomicMax(out + 1, 1);
-    atomicMax(out + 2, back1);
-    atomicMax(out + 3, back0);
+    const int SPW = 32 / NR, g = v / seg, k = g % SPW;
+    int dreq = 1, back0 = INT_MIN, dmax = 0;
+    const bool ok = for_terms<K>(S, seg, v, NR, C, [&](int st, int d, int jx, int ix) {
+        if (d == 0) {
+            back0 = max(back0, ix - jx - st);
+        } else {
+            dmax = max(dmax, d);
+            const int need = st + 1 + jx - ix;  // d * D >= need for a term inside the block
+            if (d <= k && need > 0) dreq = max(dreq, (need + d - 1) / d);
+        }
+    });
+    atomicMax(Db + g / SPW, dreq);
+    if (!ok) atomicMax(out + 0, 1);
+    atomicMax(out + 1, back0);
+    atomicMax(out + 2, dmax);
+}
+
+// pass 1b: per block and halo distance, the lead R and the read-behind window W of segment 0
+// (in segment-0 rows); out[0] = ring requirement inside the block
+template <int K>
+__global__ void k_skew_req2(Sell S, int32_t seg, int NR, int C, const int32_t* __restrict__ Db, int32_t* R,
+                            int32_t* W, int* out) {
+    const int32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= S.n) return;
+    const int SPW = 32 / NR, g = v / seg, k = g % SPW, b = g / SPW;
+    const int D = Db[b];
+    int ring = INT_MIN;
+    int Rl[MAXD], Wl[MAXD];
+    for (int d = 0; d < MAXD; ++d) Rl[d] = Wl[d] = INT_MIN;
+    for_terms<K>(S, seg, v, NR, C, [&](int st, int d, int jx, int ix) {
+        if (d == 0) return;
+        if (d <= k) {
+            ring = max(ring, ix - jx - st + d * D);  // writer row at the read minus jx
+        } else {
+            const int hd = d - k - 1;  // halo distance - 1
+            Rl[hd] = max(Rl[hd], st + 1 + jx - ix - D * k);
+            Wl[hd] = max(Wl[hd], ix + D * k - st - jx);
+        }
+    });
+    for (int d = 0; d < MAXD; ++d)
+        if (Rl[d] > INT_MIN) {
+            atomicMax(R + b * MAXD + d, Rl[d]);
+            atomicMax(W + b * MAXD + d, Wl[d]);
+        }
+    atomicMax(out, ring);
 }
 
 // pass 2: step-major items, one thread per (step, lane)
 template <int K>
-__global__ void k_skew_fill(Sell S, const double* __restrict__ dinv, int32_t seg, int32_t nseg, int32_t D,
-                            int32_t ns_full, int64_t nsteps, uint4* __restrict__ item) {
+__global__ void k_skew_fill(Sell S, const double* __restrict__ dinv, int32_t seg, int32_t nseg,
+                            const int32_t* __restrict__ Db, const int64_t* __restrict__ off, int32_t nblk, int NR,
+                            int C, int RY, int64_t nsteps, uint4* __restrict__ item) {
     const int64_t gid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (gid >= nsteps * 32) return;
     const int64_t ts = gid >> 5;
     const int lane = int(gid & 31);
-    const int k = lane >> 2, role = lane & 3;
-    const int b = int(ts / ns_full), t = int(ts - int64_t(b) * ns_full);
+    const int SPW = 32 / NR, P = NR - 1;
+    const int k = lane / NR, role = lane % NR;
+    int lo = 0, hi = nblk;  // the block holding step ts: off[b] <= ts < off[b+1]
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (off[mid] <= ts) lo = mid;
+        else hi = mid;
+    }
+    const int b = lo, t = int(ts - off[b]), D = Db[b];
     const int g = b * SPW + k;
     const int ix = t - P - D * k + role;  // the row this lane works on at step t
+    const int zero = RY * 8;
     SkewItem it{};
+    for (int q = 0; q < 4; ++q) it.o[q] = zero;
     if (g < nseg && ix >= 0 && ix < seg && int64_t(g) * seg + ix < S.n) {
-        SkewRec r;
-        int fail, dreq, back1, back0;
-        skew_record<K>(S, dinv, seg, g * seg + ix, r, fail, dreq, back1, back0);
+        const int v = g * seg + ix;
+        RowView<K> r(S, v);
+        int q = r.len - 1;
+        const bool has0 = q >= 0 && r.col(q) == v - 1 && ix > 0;
         if (role == 0) {
-            it.w[0] = r.coef[P * C];
-            it.flag = r.has0;
-            it.dinv = r.dinv;
-            it.o[0] = it.o[1] = it.o[2] = RY * 8;
+            it.w[0] = has0 ? r.val(q) : 0.0;
+            it.w[1] = K == kSkewU ? dinv[v] : 1.0;
+            it.o[0] = has0 ? 8 : 0;
         } else {
-            const int s0 = (P - role) * C;
-            for (int q = 0; q < C; ++q) {
-                it.w[q] = r.coef[s0 + q];
-                it.o[q] = r.off[s0 + q];
+            if (has0) --q;
+            const int hi = q - (role - 1) * C;  // the stage's last term
+            const int RYS = RY + 1;
+            for (int s = 0; s < C; ++s) {
+                const int kk = hi - s;
+                if (kk < 0) break;
+                const int c = r.col(kk);
+                const int gc = c / seg, jx = c - gc * seg, d = g - gc;
+                it.w[C - 1 - s] = r.val(kk);
+                it.o[C - 1 - s] = (-d * RYS + (jx & (RY - 1))) * 8;
             }
         }
-    } else {
-        it.o[0] = it.o[1] = it.o[2] = RY * 8;
     }
     const uint4* src = reinterpret_cast<const uint4*>(&it);
 #pragma unroll
@@ -441,54 +477,117 @@ __global__ void k_skew_upd(const double* __restrict__ x, double* __restrict__ u,
     u[i] = u[i] + x[v];
 }
 
+size_t smem_bytes(int NR, int dm, int ry) { return sizeof(SkewSmem) + sizeof(double) * (dm + 32 / NR) * (ry + 1); }
+
 }  // namespace
 
 bool g_skew_trace_on = false;
 unsigned long long* g_skew_trace = nullptr;
 int g_skew_trace_n = 0;
 
-bool skew_plan(const Sell& S, const double* dinv, int32_t seg, SkewKind kind, SkewPlan& plan, cudaStream_t st) {
+bool skew_plan(const Sell& S, const double* dinv, int32_t seg, SkewKind kind, int32_t max_terms, SkewPlan& plan,
+               cudaStream_t st) {
     skew_plan_free(plan);
     if (seg <= 0 || S.n == 0) return false;
-    int* d;
-    PMG_CUDA(cudaMallocAsync(&d, sizeof(int) * 4, st));
-    const int init[4] = {0, 0, INT_MIN, INT_MIN};
-    PMG_CUDA(cudaMemcpyAsync(d, init, sizeof(init), cudaMemcpyHostToDevice, st));
-    if (kind == kSkewL) k_skew_req<kSkewL><<<ceil_div(S.n, 256), 256, 0, st>>>(S, dinv, seg, d);
-    else k_skew_req<kSkewU><<<ceil_div(S.n, 256), 256, 0, st>>>(S, dinv, seg, d);
-    PMG_LAUNCH_CHECK();
-    int h[4];
-    PMG_CUDA(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, st));
-    PMG_CUDA(cudaStreamSynchronize(st));
-    PMG_CUDA(cudaFreeAsync(d, st));
-    const int D = std::max(h[0], 1);
-    // ring reuse: a value read one segment back / in the own segment must not be overwritten
-    // before its reading step (RY > D + back1, RY > back0), and D + 2 <= RY for the halo
-    const bool ok = !h[1] && D + 2 <= RY && (h[2] == INT_MIN || D + h[2] < RY) && (h[3] == INT_MIN || h[3] < RY);
-    if (!ok) return false;
+    // the smallest layout whose stages hold the longest row
+    static const int lay[][2] = {{4, 3}, {8, 4}, {16, 4}, {32, 3}, {32, 4}};  // C <= 4: SkewItem
+    int NR = 0, C = 0;
+    for (auto& l : lay)
+        if (1 + (l[0] - 1) * l[1] >= max_terms) {
+            NR = l[0];
+            C = l[1];
+            break;
+        }
+    if (!NR) return false;
+    const int SPW = 32 / NR, P = NR - 1;
     const int nseg = ceil_div(S.n, seg);
     const int nblk = ceil_div(nseg, SPW);
-    const int ns_full = seg + (SPW - 1) * D + P;
-    const int kl = nseg - 1 - (nblk - 1) * SPW;
-    const int ns_last = seg + kl * D + P;
-    const int64_t nsteps = int64_t(nblk - 1) * ns_full + ns_last;
+    int32_t *Db = nullptr, *R = nullptr, *W = nullptr;
+    int64_t* off = nullptr;
+    int* d = nullptr;
+    PMG_CUDA(cudaMalloc(&Db, sizeof(int32_t) * nblk));
+    PMG_CUDA(cudaMalloc(&R, sizeof(int32_t) * nblk * MAXD));
+    PMG_CUDA(cudaMalloc(&W, sizeof(int32_t) * nblk * MAXD));
+    PMG_CUDA(cudaMalloc(&off, sizeof(int64_t) * (nblk + 1)));
+    PMG_CUDA(cudaMalloc(&d, sizeof(int) * 4));
+    auto fail = [&] {
+        cudaFree(Db);
+        cudaFree(R);
+        cudaFree(W);
+        cudaFree(off);
+        cudaFree(d);
+        return false;
+    };
+    std::vector<int32_t> minus(size_t(nblk) * MAXD, INT_MIN);
+    PMG_CUDA(cudaMemsetAsync(Db, 0, sizeof(int32_t) * nblk, st));
+    PMG_CUDA(cudaMemcpyAsync(R, minus.data(), sizeof(int32_t) * minus.size(), cudaMemcpyHostToDevice, st));
+    PMG_CUDA(cudaMemcpyAsync(W, minus.data(), sizeof(int32_t) * minus.size(), cudaMemcpyHostToDevice, st));
+    const int init[4] = {0, INT_MIN, 0, INT_MIN};
+    PMG_CUDA(cudaMemcpyAsync(d, init, sizeof(init), cudaMemcpyHostToDevice, st));
+    if (kind == kSkewL) k_skew_req<kSkewL><<<ceil_div(S.n, 256), 256, 0, st>>>(S, seg, NR, C, Db, d);
+    else k_skew_req<kSkewU><<<ceil_div(S.n, 256), 256, 0, st>>>(S, seg, NR, C, Db, d);
+    PMG_LAUNCH_CHECK();
+    if (kind == kSkewL) k_skew_req2<kSkewL><<<ceil_div(S.n, 256), 256, 0, st>>>(S, seg, NR, C, Db, R, W, d + 3);
+    else k_skew_req2<kSkewU><<<ceil_div(S.n, 256), 256, 0, st>>>(S, seg, NR, C, Db, R, W, d + 3);
+    PMG_LAUNCH_CHECK();
+    int h[4];
+    std::vector<int32_t> hD(nblk), hR(size_t(nblk) * MAXD), hW(size_t(nblk) * MAXD);
+    PMG_CUDA(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, st));
+    PMG_CUDA(cudaMemcpyAsync(hD.data(), Db, sizeof(int32_t) * nblk, cudaMemcpyDeviceToHost, st));
+    PMG_CUDA(cudaMemcpyAsync(hR.data(), R, sizeof(int32_t) * hR.size(), cudaMemcpyDeviceToHost, st));
+    PMG_CUDA(cudaMemcpyAsync(hW.data(), W, sizeof(int32_t) * hW.size(), cudaMemcpyDeviceToHost, st));
+    PMG_CUDA(cudaStreamSynchronize(st));
+    if (h[0]) return fail();
+    const int dm = std::max(h[2], 1);
+    // rings: the own segment's back reach, what a reader inside the block still needs, and
+    // the halo window (lead + read-behind) with room for the bridge to run ahead
+    int need = std::max(h[1] + 1, h[3] + 1);
+    int64_t Dsum = 0, Dmax = 0;
+    for (int b = 0; b < nblk; ++b) {
+        Dsum += hD[b];
+        Dmax = std::max<int64_t>(Dmax, hD[b]);
+        for (int q = 0; q < MAXD; ++q)
+            if (hR[size_t(b) * MAXD + q] > INT_MIN) need = std::max(need, hR[size_t(b) * MAXD + q] + hW[size_t(b) * MAXD + q] + 32);
+    }
+    int ry = 64;
+    while (ry <= need) ry *= 2;
+    if (ry > 1024 || smem_bytes(NR, dm, ry) > 227 * 1024) return fail();
+    std::vector<int64_t> hoff(nblk + 1, 0);
+    for (int b = 0; b < nblk; ++b) {
+        const int kl = std::min(SPW - 1, nseg - 1 - b * SPW);
+        hoff[b + 1] = hoff[b] + seg + int64_t(kl) * hD[b] + P;
+    }
+    const int64_t nsteps = hoff[nblk];
+    PMG_CUDA(cudaMemcpyAsync(off, hoff.data(), sizeof(int64_t) * (nblk + 1), cudaMemcpyHostToDevice, st));
     uint4* item = nullptr;
     PMG_CUDA(cudaMalloc(&item, size_t(nsteps) * STEP_BYTES));
     const int64_t nthr = nsteps * 32;
     if (kind == kSkewL)
-        k_skew_fill<kSkewL><<<ceil_div(nthr, 256), 256, 0, st>>>(S, dinv, seg, nseg, D, ns_full, nsteps, item);
+        k_skew_fill<kSkewL><<<ceil_div(nthr, 256), 256, 0, st>>>(S, dinv, seg, nseg, Db, off, nblk, NR, C, ry, nsteps,
+                                                                 item);
     else
-        k_skew_fill<kSkewU><<<ceil_div(nthr, 256), 256, 0, st>>>(S, dinv, seg, nseg, D, ns_full, nsteps, item);
+        k_skew_fill<kSkewU><<<ceil_div(nthr, 256), 256, 0, st>>>(S, dinv, seg, nseg, Db, off, nblk, NR, C, ry, nsteps,
+                                                                 item);
     PMG_LAUNCH_CHECK();
     PMG_CUDA(cudaStreamSynchronize(st));
+    cudaFree(d);
     plan.n = S.n;
     plan.seg = seg;
-    plan.D = D;
-    plan.b1 = std::max(h[2], 1);
+    plan.D = int32_t(Dmax);
+    int lead = 0;  // the largest interior lead one segment back (reporting)
+    for (int b = nblk / 2; b < std::min(nblk, nblk / 2 + 4); ++b) lead = std::max(lead, hR[size_t(b) * MAXD]);
+    plan.lead = SPW == 1 ? lead : int32_t(Dsum / nblk);
+    plan.dm = dm;
+    plan.ry = ry;
+    plan.nr = NR;
+    plan.c = C;
     plan.nseg = nseg;
     plan.nblk = nblk;
-    plan.ns_full = ns_full;
-    plan.ns_last = ns_last;
+    plan.nsteps = nsteps;
+    plan.Db = Db;
+    plan.off = off;
+    plan.R = R;
+    plan.W = W;
     plan.item = item;
     plan.ok = true;
     return true;
@@ -496,8 +595,35 @@ bool skew_plan(const Sell& S, const double* dinv, int32_t seg, SkewKind kind, Sk
 
 void skew_plan_free(SkewPlan& plan) {
     cudaFree(plan.item);
+    cudaFree(plan.Db);
+    cudaFree(plan.off);
+    cudaFree(plan.R);
+    cudaFree(plan.W);
     plan = SkewPlan{};
 }
+
+namespace {
+template <int K, int NR, int C>
+void launch(const SkewArgs& a, int grid, int smem, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        PMG_CUDA(cudaFuncSetAttribute(k_skew<K, NR, C, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        PMG_CUDA(cudaFuncSetAttribute(k_skew<K, NR, C, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        attr = true;
+    }
+    if (a.trace) k_skew<K, NR, C, true><<<grid, NT, smem, st>>>(a);
+    else k_skew<K, NR, C, false><<<grid, NT, smem, st>>>(a);
+    PMG_LAUNCH_CHECK();
+}
+template <int K>
+void launch_kind(const SkewPlan& p, const SkewArgs& a, int grid, int smem, cudaStream_t st) {
+    if (p.nr == 4) launch<K, 4, 3>(a, grid, smem, st);
+    else if (p.nr == 8) launch<K, 8, 4>(a, grid, smem, st);
+    else if (p.nr == 16) launch<K, 16, 4>(a, grid, smem, st);
+    else if (p.c == 3) launch<K, 32, 3>(a, grid, smem, st);
+    else launch<K, 32, 4>(a, grid, smem, st);
+}
+}  // namespace
 
 void skew_sweep(const SkewOp& op, int* ticket, cudaStream_t st) {
     const SkewPlan& p = *op.plan;
@@ -505,35 +631,20 @@ void skew_sweep(const SkewOp& op, int* ticket, cudaStream_t st) {
     if (n == 0) return;
     fill_sentinel(op.out, n, st);
     PMG_CUDA(cudaMemsetAsync(ticket, 0, sizeof(int), st));
-    const int nseg = ceil_div(n, p.seg);
-    const int nblk = ceil_div(nseg, SPW);
     static int nsm = 0;
     if (!nsm) {
         int dev = 0;
         PMG_CUDA(cudaGetDevice(&dev));
         PMG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     }
-    const int smem = int(sizeof(SkewSmem));
-    static bool attr = false;
-    if (!attr) {
-        PMG_CUDA(cudaFuncSetAttribute(k_skew<kSkewL, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        PMG_CUDA(cudaFuncSetAttribute(k_skew<kSkewU, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        PMG_CUDA(cudaFuncSetAttribute(k_skew<kSkewL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        PMG_CUDA(cudaFuncSetAttribute(k_skew<kSkewU, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        attr = true;
-    }
-    static int dbg = -1;
-    if (dbg < 0) {
-        const char* e = getenv("PMG_SKEW_DBG");
-        dbg = e ? atoi(e) : 0;
-    }
-    SkewArgs a{p.item, op.rhs, op.out, n, p.seg, nseg, p.D, p.b1, p.ns_full, ticket, nullptr, dbg};
+    const int smem = int(smem_bytes(p.nr, p.dm, p.ry));
+    SkewArgs a{p.item, op.rhs, op.out, p.Db, p.off, p.R, p.W, n, p.seg, p.nseg, p.dm, p.ry, ticket, nullptr};
     if (g_skew_trace_on) {  // one-shot trace of the next sweep (diagnostics)
         g_skew_trace_on = false;
         cudaFree(g_skew_trace);
-        PMG_CUDA(cudaMalloc(&g_skew_trace, sizeof(unsigned long long) * 8 * nblk));
-        PMG_CUDA(cudaMemsetAsync(g_skew_trace, 0, sizeof(unsigned long long) * 8 * nblk, st));
-        g_skew_trace_n = nblk;
+        PMG_CUDA(cudaMalloc(&g_skew_trace, sizeof(unsigned long long) * 8 * p.nblk));
+        PMG_CUDA(cudaMemsetAsync(g_skew_trace, 0, sizeof(unsigned long long) * 8 * p.nblk, st));
+        g_skew_trace_n = p.nblk;
         a.trace = g_skew_trace;
     }
     static int grid_cap = -1;  // tests: fewer CTAs than blocks (CTAs then loop over blocks)
@@ -541,15 +652,10 @@ void skew_sweep(const SkewOp& op, int* ticket, cudaStream_t st) {
         const char* e = getenv("PMG_SKEW_GRID");
         grid_cap = e ? std::max(1, atoi(e)) : 0;
     }
-    const int grid = std::min(std::min(nblk, nsm), grid_cap > 0 ? grid_cap : nsm);
-    if (a.trace) {
-        if (op.kind == kSkewL) k_skew<kSkewL, true><<<grid, 96, smem, st>>>(a);
-        else k_skew<kSkewU, true><<<grid, 96, smem, st>>>(a);
-    } else {
-        if (op.kind == kSkewL) k_skew<kSkewL, false><<<grid, 96, smem, st>>>(a);
-        else k_skew<kSkewU, false><<<grid, 96, smem, st>>>(a);
-    }
-    PMG_LAUNCH_CHECK();
+    const int per_sm = std::max(1, int((227 * 1024) / (smem + 1024)));
+    const int grid = std::min(std::min(p.nblk, nsm * per_sm), grid_cap > 0 ? grid_cap : INT_MAX);
+    if (op.kind == kSkewL) launch_kind<kSkewL>(p, a, grid, smem, st);
+    else launch_kind<kSkewU>(p, a, grid, smem, st);
     if (op.kind == kSkewU) {
         k_skew_upd<<<ceil_div(n, 256), 256, 0, st>>>(op.out, op.upd, n);
         PMG_LAUNCH_CHECK();

@@ -1,5 +1,5 @@
-// Skewed-warp wavefront sweeps for factors with short rows and short reach (the p=1
-// h-levels: <= 9 off-diagonal entries per row, reach one grid row back).
+// Skewed-warp wavefront sweeps for sparse triangular solves on tensor-grid orderings
+// (rows of up to 125 terms reaching up to 8 grid rows back: every p-level of the configs).
 #pragma once
 
 #include "sell.cuh"
@@ -8,36 +8,33 @@ namespace pmg {
 
 enum SkewKind : int { kSkewL = 0, kSkewU = 1 };
 
-// Per-row record, staged to shared memory with cp.async (7 x 16 B).  The row's terms are
-// pre-assigned to pipeline stages: stage s (s = kSkewP..1) is accumulated s steps before the
-// row is finalised, kSkewC terms per stage, in the oracle's ascending order; stage 0 is the
-// single v-1 term, taken from a register.  Padding slots have coef 0 and point at a zero cell.
-constexpr int kSkewP = 3;
-constexpr int kSkewC = 3;
-constexpr int kSkewSlots = kSkewP * kSkewC + 1;
-struct __align__(16) SkewRec {
-    double coef[kSkewSlots];       // slots [0,C): stage P ... [(P-1)C, PC): stage 1; slot PC: stage 0
-    int32_t off[kSkewSlots - 1];   // byte offset of the term's value relative to the lane's ring
-    int32_t has0;                  // slot PC holds the v-1 term (taken from a register)
-    double dinv;                   // U: reciprocal diagonal
-};
-static_assert(sizeof(SkewRec) == 128, "SkewRec layout");
-
 // The sweep kernel reads per-(step, lane) items (a lane's stage data, 48 B) stored step-major
-// per 8-segment warp block, [3 x 16-B chunks][32 lanes] per step, so one bulk copy moves a
-// group of steps for the whole warp.  Block b starts at step offset b * ns_full.
+// per warp block, [3 x 16-B chunks][32 lanes] per step, so one bulk copy moves a group of
+// steps for the whole warp.  Block b's steps start at off[b].
 struct SkewPlan {
-    int32_t n = 0, seg = 0, D = 0, b1 = 1;  // b1: how far behind its row a term one segment back may lie
-    int32_t nseg = 0, nblk = 0, ns_full = 0, ns_last = 0;
-    uint4* item = nullptr;     // [(nblk-1)*ns_full + ns_last][3][32]
+    int32_t n = 0, seg = 0;
+    int32_t D = 0;             // largest lane skew of a block (steps; reporting)
+    int32_t lead = 0;          // typical lag between consecutive segments (reporting)
+    int32_t dm = 1;            // segments back a term reaches
+    int32_t ry = 64;           // ring length (rows) per segment in shared memory
+    int32_t nr = 4, c = 3;     // lanes per segment (stages + 1), terms per lane and stage
+    int32_t nseg = 0, nblk = 0;
+    int64_t nsteps = 0;
+    int32_t* Db = nullptr;     // [nblk] lane skew per block (the boundary blocks need more)
+    int64_t* off = nullptr;    // [nblk+1] step offsets of the blocks in the item stream
+    int32_t* R = nullptr;      // [nblk][8] lead a halo segment needs over the block's segment 0
+    int32_t* W = nullptr;      // [nblk][8] read-behind window of the halo rings
+    uint4* item = nullptr;     // [nsteps][3][32]
     bool ok = false;
 };
 
-// Build the records of the v-ordered factor S (segment length seg) and the lane skew D.
-// Returns false (plan.ok = false, nothing allocated) when a row does not fit: more than
-// kSkewSlots terms, an entry more than one segment back, or a term whose value would not be
-// ready at its stage.
-bool skew_plan(const Sell& S, const double* dinv, int32_t seg, SkewKind kind, SkewPlan& plan, cudaStream_t st);
+// Build the step-major items of the v-ordered factor S (segment length seg; longest row
+// max_terms off-diagonal terms) and choose the layout and the lane skew D.  Returns false
+// (nothing allocated) when a row does not fit: more terms than the widest layout, an entry
+// more than 8 segments back, a term whose value would not be final at its stage, or rings
+// beyond shared memory.
+bool skew_plan(const Sell& S, const double* dinv, int32_t seg, SkewKind kind, int32_t max_terms, SkewPlan& plan,
+               cudaStream_t st);
 void skew_plan_free(SkewPlan& plan);
 
 struct SkewOp {

@@ -3,10 +3,12 @@ import ctypes, sys, time, numpy as np
 sys.path.insert(0, '.')
 from paper_1901_01685_b200 import pmg, problems as P
 h = int(sys.argv[1]) if len(sys.argv) > 1 else 10
+deg = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 L = pmg.lib()
 L.pmg_debug_skew_trace.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int]
-spec = P.make_spec(geometry="annulus", rhs="one", degrees=(2, 1), h_exp=h)
-A = P.build(spec).hlevels[0].A
+spec = P.make_spec(geometry="annulus", rhs="one", degrees=(max(deg, 2), 1), h_exp=h)
+pb = P.build(spec)
+A = pb.hlevels[0].A if deg == 1 else pb.plevels[0].A
 n = A.nrows
 F = pmg.ilut_factorize(A, 1e-12, 1.0, "none")
 print(F.stats())
@@ -17,8 +19,8 @@ for _ in range(K): pmg.ilut_apply(F, r)
 print("ilut_apply (L+U sweeps + copies) ms", (time.perf_counter() - t0) / K * 1e3)
 L.pmg_debug_skew_trace(1, None, 0)
 pmg.ilut_apply(F, r)
-buf = (ctypes.c_ulonglong * 4096)()
-nb = L.pmg_debug_skew_trace(-1, buf, 4096)
+buf = (ctypes.c_ulonglong * 65536)()
+nb = L.pmg_debug_skew_trace(-1, buf, 65536)
 tr = np.array(buf[:8 * nb], dtype=np.int64).reshape(nb, 8)
 t0 = tr[:, 0].min()
 print("blocks", nb, "sweep span us", (tr[:, 1].max() - t0) / 1e3)
