@@ -187,17 +187,20 @@ __global__ void __launch_bounds__(NT) k_skew(SkewArgs a) {
                     Wq[d] = d < DM ? a.W[blk * MAXD + d] : 0;
                     f[d] = (Rq[d] > INT_MIN / 2 && g0 - 1 - d >= 0) ? 0 : S;  // halo rows nobody reads: done
                 }
-                int pub = INT_MIN / 2;
+                int pub = INT_MIN / 2, idle = 0;
                 unsigned ns = 16;
                 while (pub < INT_MAX / 2) {
                     const int cons = ld_vol_s(&sm.cons_ix);
+                    // rows further back are polled only while they may bind: their producers ran
+                    // earlier, so they are usually far ahead of what segment 0 needs
+                    const int lim = f[0] < S ? f[0] - Rq[0] + 32 : INT_MAX / 2;
                     double v[MAXD];
 #pragma unroll
                     for (int d = 0; d < MAXD; ++d) {  // halo distance delta = d + 1: all polls in flight at once
                         v[d] = sentinel();
                         const int cap = cons - Wq[d] + RY - f[d];  // ring slots free
                         const int j = f[d] + lane;
-                        if (d < DM && f[d] < S && lane < cap && j < S)
+                        if (d < DM && f[d] < S && lane < cap && j < S && (d == 0 || f[d] - Rq[d] <= lim))
                             v[d] = ld_relaxed_nb(a.out + int64_t(g0 - 1 - d) * S + j);
                     }
                     bool moved = false;
@@ -208,6 +211,8 @@ __global__ void __launch_bounds__(NT) k_skew(SkewArgs a) {
                             const unsigned ok = __ballot_sync(FULL, !is_sentinel(v[d]));
                             const int cnt = ok == FULL ? 32 : __ffs(~ok) - 1;
                             if (lane < cnt) Ybase[(DM - 1 - d) * RYS + ((f[d] + lane) & (RY - 1))] = v[d];
+                            if (TR && a.trace && d == 0 && f[d] <= 200 && f[d] + cnt > 200 && lane == 0)
+                                a.trace[(blk - 1) * 8 + 5] = gtimer();
                             f[d] += cnt;
                             moved = moved || cnt > 0;
                             if (f[d] < S) h = min(h, f[d] - Rq[d]);
@@ -216,11 +221,14 @@ __global__ void __launch_bounds__(NT) k_skew(SkewArgs a) {
                     __syncwarp();
                     if (h > pub) {
                         if (lane == 0) st_rel_cta(&sm.halo_ready, h);
+                        if (TR && a.trace && lane == 0 && f[0] > 200 && a.trace[(blk - 1) * 8 + 6] == 0)
+                            a.trace[(blk - 1) * 8 + 6] = gtimer();
                         pub = h;
                     }
-                    if (moved) {
+                    if (moved) {  // spin while values flow (this warp has its own scheduler slot)
                         ns = 16;
-                    } else {
+                        idle = 0;
+                    } else if (++idle > 8) {
                         __nanosleep(ns);
                         ns = min(ns * 2, 256u);
                     }
@@ -297,6 +305,7 @@ __global__ void __launch_bounds__(NT) k_skew(SkewArgs a) {
                         } while (hr < t - P);
                         if (TR && a.trace && lane == 0) a.trace[blk * 8 + 2] += clock64() - w0;
                     }
+                    if (TR && a.trace && lane == 0 && t - P == 200 - 46) a.trace[(blk - 1) * 8 + 7] = gtimer();
                 }
                 __syncwarp();
                 double y[C];
@@ -314,6 +323,7 @@ __global__ void __launch_bounds__(NT) k_skew(SkewArgs a) {
                 if (role == 0 && ix >= 0 && ix < rows) {
                     Yo[ix & (RY - 1)] = x;
                     st_relaxed(a.out + lo + ix, x);
+                    if (TR && a.trace && k == SPW - 1 && ix == 200) a.trace[blk * 8 + 4] = gtimer();
                 }
                 xprev = x;
                 if (g0 > 0) hr = ld_vol_s(&sm.halo_ready);  // for the next step's test

@@ -26,7 +26,7 @@ t0 = tr[:, 0].min()
 print("blocks", nb, "sweep span us", (tr[:, 1].max() - t0) / 1e3)
 for b in range(0, nb, max(1, nb // 12)):
     if b + 1 < nb and tr[b, 4]:
-        print(f"  hop at row 200: store->bridge {(tr[b,5]-tr[b,4])/1e3:.2f} us, store->sweep needs {(tr[b,6]-tr[b,4])/1e3:.2f} us, ->sweep has {(tr[b,7]-tr[b,4])/1e3:.2f} us")
+        print(f"  hop at row 200: store->bridge sees {(tr[b,5]-tr[b,4])/1e3:.2f} us, ->published {(tr[b,6]-tr[b,4])/1e3:.2f} us, ->next block at row 154 {(tr[b,7]-tr[b,4])/1e3:.2f} us")
     print(f"blk {b}: claim {(tr[b,0]-t0)/1e3:9.1f} us end {(tr[b,1]-t0)/1e3:9.1f} us dur {(tr[b,1]-tr[b,0])/1e3:8.1f} halo wait {tr[b,2]/1965:.1f} us bridge polls {tr[b,3]}")
 
 import os
