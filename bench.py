@@ -270,7 +270,8 @@ def main():
     roof = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_kind, "bytes_per_launch": bytes_dom,
             "ms_per_launch": per_launch_ms, "launches": launches_dom,
-            "note": "triangular sweeps are bounded by their dependency depth (see 'triangular'), not by HBM"}
+            "note": "triangular sweeps are bounded by their dependency depth (see 'triangular') and the per-segment "
+                    "lead of the skewed-warp wavefront, not by HBM"}
     # the HBM-bound kernel of the cycle (residual SpMV), for kernel quality
     if la.get("resid_fine", 0) > 0:
         r_ms = ms["resid_fine"] / la["resid_fine"]
@@ -318,7 +319,12 @@ def main():
         fs = ab["factor_stats"]
         line["triangular"] = {"levels_L": fs["levels_L"], "levels_U": fs["levels_U"],
                               "rows_per_level_L": fs["rows_per_level_L"], "rows_per_level_U": fs["rows_per_level_U"],
-                              "nnz_L": fs["nnz_L"], "nnz_U": fs["nnz_U"]}
+                              "nnz_L": fs["nnz_L"], "nnz_U": fs["nnz_U"], "sweep_kernel": fs.get("sweep"),
+                              "segment_rows": fs.get("segment"),
+                              "steps_per_segment_LU": list(fs.get("skew_D", ())),
+                              "note": "skewed-warp wavefront: one grid row per segment, consecutive segments "
+                                      "lag by steps_per_segment steps; the DAG depth per segment is "
+                                      "levels / (n / segment_rows)"}
     print(json.dumps(line), flush=True)
 
 
@@ -332,7 +338,11 @@ def ncu_traffic(dom, args):
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "round1", "traffic.json")
     if args.config != 5 or args.smoother != "ilut" or not os.path.exists(path):
         return None, None
-    rec = json.load(open(path)).get(NCU_KERNEL.get(dom, ""))
+    tab = json.load(open(path))
+    rec = tab.get(NCU_KERNEL.get(dom, ""))
+    if not rec:  # skewed-warp sweeps: the template arguments carry the layout
+        pre = {"lsolve_fine": "k_skew<0", "usolve_fine": "k_skew<1"}.get(dom)
+        rec = next((v for k, v in tab.items() if pre and pre in k), None)
     if not rec:
         return None, None
     return rec["dram_bytes_per_launch"], "profiles/round1/traffic.json (ncu --set full, config 5 ILUT)"

@@ -7,5 +7,5 @@ PMG_PROFILE_REGION=1 $B > gpurun_out/prof_plain.json 2> gpurun_out/prof_plain.er
 PMG_PROFILE_REGION=1 timeout 1500 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/launches.csv $B > gpurun_out/ncu_launches.log 2>&1; echo "launch list rc=$?"
 PMG_PROFILE_REGION=1 timeout 1500 ncu --profile-from-start off --set full --import-source on --clock-control none \
-    -k regex:"^k_chain$|k_rowop" -c 4 -o gpurun_out/prof_full $B > gpurun_out/ncu_full.log 2>&1; echo "full rc=$?"
+    --kernel-name-base function -k regex:"^k_skew$|^k_chain$|^k_rowop$" -c 6 -o gpurun_out/prof_full $B > gpurun_out/ncu_full.log 2>&1; echo "full rc=$?"
 ls -la gpurun_out | tail -8

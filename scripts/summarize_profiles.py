@@ -10,11 +10,17 @@ usage: python scripts/summarize_profiles.py gpurun_out profiles/round1
 import collections
 import csv
 import io
+import re
 import json
 import os
 import shutil
 import subprocess
 import sys
+
+
+def kname(full):
+    """kernel name without the parameter list; template casts like (int)0 are dropped first"""
+    return re.sub(r"\((?:int|bool|unsigned int)\)", "", full).split("(")[0].strip()
 
 
 def launch_summary(csv_path, out_path, cmd):
@@ -30,7 +36,7 @@ def launch_summary(csv_path, out_path, cmd):
         v = float(r[iv].replace(",", ""))
         unit = r[iu]
         ms = v / 1e6 if unit == "ns" else v / 1e3 if unit == "us" else v if unit == "ms" else v * 1e3
-        name = r[ik].split("(")[0]
+        name = kname(r[ik])
         agg[name][0] += ms
         agg[name][1] += 1
     total = sum(a[0] for a in agg.values())
@@ -67,13 +73,13 @@ def full_summary(rep, out_txt, out_json):
 
     traffic = collections.defaultdict(list)
     with open(out_txt, "w") as fh:
-        fh.write("ncu --set full --clock-control none --import-source on (first launches of k_chain / k_rowop in the "
-                 "timed region)\n")
+        fh.write("ncu --set full --clock-control none --import-source on (first launches of the sweep kernels / "
+                 "k_rowop in the timed region)\n")
         fh.write("kernel | duration ms | DRAM read MB | DRAM write MB | DRAM GB/s | L2 hit % | regs | grid x block\n")
         for r in rows[2:]:
             if len(r) != len(hdr):
                 continue
-            name = r[hdr.index("Kernel Name")].split("(")[0]
+            name = kname(r[hdr.index("Kernel Name")])
             d = val(r, "gpu__time_duration.sum")
             rd = val(r, "dram__bytes_read.sum") or 0.0
             wr = val(r, "dram__bytes_write.sum") or 0.0
