@@ -120,6 +120,9 @@ struct pmg_csr_s {
     int32_t* gs_split = nullptr;
     int32_t gs_gap = 0;
     bool gs_chain = false;        // chained GS sweep (else level-scheduled)
+    bool gs_skew = false;         // skewed-warp GS sweep (default for tensor-grid orderings)
+    SkewPlan gs_plan;
+    double* gs_su = nullptr;      // upper sums over the old values (skew GS pre-pass)
     ~pmg_csr_s() {
         A.free();
         sell_free(S);
@@ -129,6 +132,8 @@ struct pmg_csr_s {
             cudaFree(gs_diag);
             cudaFree(gs_nlow);
             cudaFree(gs_split);
+            skew_plan_free(gs_plan);
+            cudaFree(gs_su);
         }
     }
 };
@@ -188,7 +193,10 @@ void apply_factor(pmg_factor_s* F, const double* r, double* y, double* x, double
 }
 
 void gs_apply(pmg_csr_s* A, const double* f, const double* uo, double* un, int* ticket, cudaStream_t st) {
-    if (A->gs_chain) {
+    if (A->gs_skew) {
+        SkewOp g{kSkewGS, &A->gs_plan, f, un, nullptr, &A->gs, A->gs_nlow, uo, A->gs_su};
+        skew_sweep(g, ticket, st);
+    } else if (A->gs_chain) {
         ChainOp g{kChainGS, &A->gs, A->gs_diag, A->gs_nlow, A->gs_split, nullptr, f, uo, un, nullptr, A->seg, 8, A->gs_gap};
         chain_sweep(g, ticket, st);
     } else {
@@ -245,6 +253,16 @@ void ensure_gs(pmg_csr_s* h, cudaStream_t st) {
     }
     h->gs_zero_row = zr;
     reciprocal_inplace(h->gs_diag, n, st);
+    const char* sk = getenv("PMG_SKEW");
+    if (h->gs_chain && !(sk && sk[0] == '0')) {  // skewed-warp GS sweeps over the lower entries
+        std::vector<int32_t> nl(n);
+        PMG_CUDA(cudaMemcpyAsync(nl.data(), h->gs_nlow, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
+        PMG_CUDA(cudaStreamSynchronize(st));
+        int32_t mx = 0;
+        for (int32_t v : nl) mx = std::max(mx, v);
+        h->gs_skew = skew_plan(h->gs, h->gs_diag, h->seg, kSkewGS, mx, h->gs_plan, st, h->gs_nlow);
+        if (h->gs_skew) h->gs_su = dalloc<double>(n);
+    }
     h->gs_ready = true;
 }
 

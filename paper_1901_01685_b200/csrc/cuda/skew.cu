@@ -54,6 +54,7 @@ static_assert(sizeof(SkewItem) == ICH * 16, "SkewItem layout");
 struct SkewSmem {
     uint4 item[PF][ICH][32];  // [step slot][16-B chunk][lane]: conflict-free 128-bit reads
     double rhs[PF][32];
+    double su[PF][32];              // Gauss-Seidel: the rows' upper sums over the old values
     unsigned long long bar[NG];     // items of a group have landed (bulk copy)
     unsigned long long rfull[NG];   // right-hand sides of a group are in (stager warp)
     unsigned long long rempty[NG];  // a group's slots were consumed (sweep warp)
@@ -73,6 +74,7 @@ struct SkewArgs {
     const int64_t* off;       // [nblk+1] first step of the block in the item stream
     const int32_t* R;         // [nblk][MAXD] lead (rows) a halo segment needs over segment 0
     const int32_t* W;         // [nblk][MAXD] how far behind segment 0 a halo value is still read
+    const double* su;         // Gauss-Seidel upper sums (natural order)
     int32_t n, seg, nseg, dm, ry;
     int* ticket;
     unsigned long long* trace;  // optional: per block [claim, end, halo wait cycles, bridge polls, ...]
@@ -167,7 +169,8 @@ __global__ void __launch_bounds__(NT) k_skew(SkewArgs a) {
                         const bool in = gg < a.nseg && ix >= 0 && ix < S && lo2 + ix < n;
                         const int64_t v = lo2 + ix;
                         sm.rhs[slot * G + e / SPW][kk * NR] =
-                            in ? a.rhs[K == kSkewL ? v : int64_t(n) - 1 - v] : 0.0;
+                            in ? a.rhs[K == kSkewU ? int64_t(n) - 1 - v : v] : 0.0;
+                        if (K == kSkewGS) sm.su[slot * G + e / SPW][kk * NR] = in ? a.su[v] : 0.0;
                     }
                 }
                 __syncwarp();
@@ -257,7 +260,7 @@ __global__ void __launch_bounds__(NT) k_skew(SkewArgs a) {
         const char* Yb = reinterpret_cast<const char*>(Ybase + (DM + k) * RYS);
         double* Yo = Ybase + (DM + k) * RYS;
         struct Pre {
-            double w[4], rhs;
+            double w[4], rhs, su;
             int o[4];
         };
         auto fetch = [&](int t, Pre& f) {  // static data of step t from the ring
@@ -272,6 +275,7 @@ __global__ void __launch_bounds__(NT) k_skew(SkewArgs a) {
             f.o[2] = int(c2.z);
             f.o[3] = int(c2.w);
             f.rhs = sm.rhs[t & (PF - 1)][lane];
+            if (K == kSkewGS) f.su = sm.su[t & (PF - 1)][lane];
         };
         auto group_wait = [&](unsigned q) {  // items and right-hand sides of group q are in
             if (q < nq) {
@@ -319,7 +323,9 @@ __global__ void __launch_bounds__(NT) k_skew(SkewArgs a) {
                 for (int q = 1; q < C; ++q) r = r + f.w[q] * y[q];
                 res = r;
                 // stage-0 lanes: finalise (r1 is their complete row sum, w[1] their 1/diagonal)
-                const double x = K == kSkewL ? f.rhs - r1 : (f.rhs - r1) * f.w[1];
+                const double x = K == kSkewL    ? f.rhs - r1
+                                 : K == kSkewU ? (f.rhs - r1) * f.w[1]
+                                               : ((f.rhs - r1) - f.su) * f.w[1];  // GS: SPEC order
                 if (role == 0 && ix >= 0 && ix < rows) {
                     Yo[ix & (RY - 1)] = x;
                     st_relaxed(a.out + lo + ix, x);
@@ -346,7 +352,9 @@ struct RowView {
     int v, n, len;
     int64_t base;
     int li;
-    __device__ RowView(const Sell& s, int v_) : S(s), v(v_), n(s.n), len(s.len[v_]), base(s.off[v_ >> 5]), li(v_ & 31) {}
+    // Gauss-Seidel: only the lower entries (the first nlow[v]) are terms of the sweep
+    __device__ RowView(const Sell& s, int v_, const int32_t* nlow)
+        : S(s), v(v_), n(s.n), len(K == kSkewGS ? nlow[v_] : s.len[v_]), base(s.off[v_ >> 5]), li(v_ & 31) {}
     __device__ int col(int k) const { return vcol<K>(S.col[base + (k >> 2) * 128 + li * 4 + (k & 3)], n); }
     __device__ double val(int k) const { return S.val[base + (k >> 1) * 64 + li * 2 + (k & 1)]; }
 };
@@ -355,8 +363,8 @@ struct RowView {
 // term; returns false if a term does not fit the layout (more than P stages, own value not
 // final by its stage, not ascending, more than MAXD segments back).
 template <int K, class F>
-__device__ bool for_terms(const Sell& S, int32_t seg, int v, int NR, int C, F&& f) {
-    RowView<K> r(S, v);
+__device__ bool for_terms(const Sell& S, const int32_t* nlow, int32_t seg, int v, int NR, int C, F&& f) {
+    RowView<K> r(S, v, nlow);
     const int g = v / seg, ix = v - g * seg, P = NR - 1;
     int q = r.len - 1;
     if (q >= 0 && r.col(q) == v - 1 && ix > 0) --q;  // stage 0: the v-1 term
@@ -379,12 +387,12 @@ __device__ bool for_terms(const Sell& S, int32_t seg, int v, int NR, int C, F&& 
 // pass 1a: per block, the lane skew D_b covering every term inside the block; global failure,
 // own-segment back reach and segments-back reach.  out[0] fail, out[1] back0, out[2] dmax
 template <int K>
-__global__ void k_skew_req(Sell S, int32_t seg, int NR, int C, int32_t* Db, int* out) {
+__global__ void k_skew_req(Sell S, const int32_t* nlow, int32_t seg, int NR, int C, int32_t* Db, int* out) {
     const int32_t v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= S.n) return;
     const int SPW = 32 / NR, g = v / seg, k = g % SPW;
     int dreq = 1, back0 = INT_MIN, dmax = 0;
-    const bool ok = for_terms<K>(S, seg, v, NR, C, [&](int st, int d, int jx, int ix) {
+    const bool ok = for_terms<K>(S, nlow, seg, v, NR, C, [&](int st, int d, int jx, int ix) {
         if (d == 0) {
             back0 = max(back0, ix - jx - st);
         } else {
@@ -402,8 +410,8 @@ __global__ void k_skew_req(Sell S, int32_t seg, int NR, int C, int32_t* Db, int*
 // pass 1b: per block and halo distance, the lead R and the read-behind window W of segment 0
 // (in segment-0 rows); out[0] = ring requirement inside the block
 template <int K>
-__global__ void k_skew_req2(Sell S, int32_t seg, int NR, int C, const int32_t* __restrict__ Db, int32_t* R,
-                            int32_t* W, int* out) {
+__global__ void k_skew_req2(Sell S, const int32_t* nlow, int32_t seg, int NR, int C,
+                            const int32_t* __restrict__ Db, int32_t* R, int32_t* W, int* out) {
     const int32_t v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= S.n) return;
     const int SPW = 32 / NR, g = v / seg, k = g % SPW, b = g / SPW;
@@ -411,7 +419,7 @@ __global__ void k_skew_req2(Sell S, int32_t seg, int NR, int C, const int32_t* _
     int ring = INT_MIN;
     int Rl[MAXD], Wl[MAXD];
     for (int d = 0; d < MAXD; ++d) Rl[d] = Wl[d] = INT_MIN;
-    for_terms<K>(S, seg, v, NR, C, [&](int st, int d, int jx, int ix) {
+    for_terms<K>(S, nlow, seg, v, NR, C, [&](int st, int d, int jx, int ix) {
         if (d == 0) return;
         if (d <= k) {
             ring = max(ring, ix - jx - st + d * D);  // writer row at the read minus jx
@@ -431,7 +439,8 @@ __global__ void k_skew_req2(Sell S, int32_t seg, int NR, int C, const int32_t* _
 
 // pass 2: step-major items, one thread per (step, lane)
 template <int K>
-__global__ void k_skew_fill(Sell S, const double* __restrict__ dinv, int32_t seg, int32_t nseg,
+__global__ void k_skew_fill(Sell S, const int32_t* __restrict__ nlow, const double* __restrict__ dinv, int32_t seg,
+                            int32_t nseg,
                             const int32_t* __restrict__ Db, const int64_t* __restrict__ off, int32_t nblk, int NR,
                             int C, int RY, int64_t nsteps, uint4* __restrict__ item) {
     const int64_t gid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -454,12 +463,12 @@ __global__ void k_skew_fill(Sell S, const double* __restrict__ dinv, int32_t seg
     for (int q = 0; q < 4; ++q) it.o[q] = zero;
     if (g < nseg && ix >= 0 && ix < seg && int64_t(g) * seg + ix < S.n) {
         const int v = g * seg + ix;
-        RowView<K> r(S, v);
+        RowView<K> r(S, v, nlow);
         int q = r.len - 1;
         const bool has0 = q >= 0 && r.col(q) == v - 1 && ix > 0;
         if (role == 0) {
             it.w[0] = has0 ? r.val(q) : 0.0;
-            it.w[1] = K == kSkewU ? dinv[v] : 1.0;
+            it.w[1] = K == kSkewL ? 1.0 : dinv[v];
             it.o[0] = has0 ? 8 : 0;
         } else {
             if (has0) --q;
@@ -480,6 +489,20 @@ __global__ void k_skew_fill(Sell S, const double* __restrict__ dinv, int32_t seg
     for (int c = 0; c < ICH; ++c) item[(ts * ICH + c) * 32 + lane] = src[c];
 }
 
+// Gauss-Seidel pre-pass: su[v] = sum over the upper entries of a_vj * u_old[j], ascending
+// from +0 (the oracle's S_U order)
+__global__ void k_skew_gs_su(Sell S, const int32_t* __restrict__ nlow, const double* __restrict__ old,
+                             double* __restrict__ su) {
+    const int32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= S.n) return;
+    const int64_t base = S.off[v >> 5];
+    const int li = v & 31, len = S.len[v];
+    double s = 0.0;
+    for (int k = nlow[v]; k < len; ++k)
+        s = s + S.val[base + (k >> 1) * 64 + li * 2 + (k & 1)] * old[S.col[base + (k >> 2) * 128 + li * 4 + (k & 3)]];
+    su[v] = s;
+}
+
 __global__ void k_skew_upd(const double* __restrict__ x, double* __restrict__ u, int32_t n) {
     const int32_t v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= n) return;
@@ -496,7 +519,7 @@ unsigned long long* g_skew_trace = nullptr;
 int g_skew_trace_n = 0;
 
 bool skew_plan(const Sell& S, const double* dinv, int32_t seg, SkewKind kind, int32_t max_terms, SkewPlan& plan,
-               cudaStream_t st) {
+               cudaStream_t st, const int32_t* nlow) {
     skew_plan_free(plan);
     if (seg <= 0 || S.n == 0) return false;
     // the smallest layout whose stages hold the longest row
@@ -534,11 +557,14 @@ bool skew_plan(const Sell& S, const double* dinv, int32_t seg, SkewKind kind, in
     PMG_CUDA(cudaMemcpyAsync(W, minus.data(), sizeof(int32_t) * minus.size(), cudaMemcpyHostToDevice, st));
     const int init[4] = {0, INT_MIN, 0, INT_MIN};
     PMG_CUDA(cudaMemcpyAsync(d, init, sizeof(init), cudaMemcpyHostToDevice, st));
-    if (kind == kSkewL) k_skew_req<kSkewL><<<ceil_div(S.n, 256), 256, 0, st>>>(S, seg, NR, C, Db, d);
-    else k_skew_req<kSkewU><<<ceil_div(S.n, 256), 256, 0, st>>>(S, seg, NR, C, Db, d);
+    const int nb = ceil_div(S.n, 256);
+    if (kind == kSkewL) k_skew_req<kSkewL><<<nb, 256, 0, st>>>(S, nlow, seg, NR, C, Db, d);
+    else if (kind == kSkewU) k_skew_req<kSkewU><<<nb, 256, 0, st>>>(S, nlow, seg, NR, C, Db, d);
+    else k_skew_req<kSkewGS><<<nb, 256, 0, st>>>(S, nlow, seg, NR, C, Db, d);
     PMG_LAUNCH_CHECK();
-    if (kind == kSkewL) k_skew_req2<kSkewL><<<ceil_div(S.n, 256), 256, 0, st>>>(S, seg, NR, C, Db, R, W, d + 3);
-    else k_skew_req2<kSkewU><<<ceil_div(S.n, 256), 256, 0, st>>>(S, seg, NR, C, Db, R, W, d + 3);
+    if (kind == kSkewL) k_skew_req2<kSkewL><<<nb, 256, 0, st>>>(S, nlow, seg, NR, C, Db, R, W, d + 3);
+    else if (kind == kSkewU) k_skew_req2<kSkewU><<<nb, 256, 0, st>>>(S, nlow, seg, NR, C, Db, R, W, d + 3);
+    else k_skew_req2<kSkewGS><<<nb, 256, 0, st>>>(S, nlow, seg, NR, C, Db, R, W, d + 3);
     PMG_LAUNCH_CHECK();
     int h[4];
     std::vector<int32_t> hD(nblk), hR(size_t(nblk) * MAXD), hW(size_t(nblk) * MAXD);
@@ -572,12 +598,13 @@ bool skew_plan(const Sell& S, const double* dinv, int32_t seg, SkewKind kind, in
     uint4* item = nullptr;
     PMG_CUDA(cudaMalloc(&item, size_t(nsteps) * STEP_BYTES));
     const int64_t nthr = nsteps * 32;
+    const int nf = ceil_div(nthr, 256);
     if (kind == kSkewL)
-        k_skew_fill<kSkewL><<<ceil_div(nthr, 256), 256, 0, st>>>(S, dinv, seg, nseg, Db, off, nblk, NR, C, ry, nsteps,
-                                                                 item);
+        k_skew_fill<kSkewL><<<nf, 256, 0, st>>>(S, nlow, dinv, seg, nseg, Db, off, nblk, NR, C, ry, nsteps, item);
+    else if (kind == kSkewU)
+        k_skew_fill<kSkewU><<<nf, 256, 0, st>>>(S, nlow, dinv, seg, nseg, Db, off, nblk, NR, C, ry, nsteps, item);
     else
-        k_skew_fill<kSkewU><<<ceil_div(nthr, 256), 256, 0, st>>>(S, dinv, seg, nseg, Db, off, nblk, NR, C, ry, nsteps,
-                                                                 item);
+        k_skew_fill<kSkewGS><<<nf, 256, 0, st>>>(S, nlow, dinv, seg, nseg, Db, off, nblk, NR, C, ry, nsteps, item);
     PMG_LAUNCH_CHECK();
     PMG_CUDA(cudaStreamSynchronize(st));
     cudaFree(d);
@@ -618,6 +645,7 @@ void launch(const SkewArgs& a, int grid, int smem, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
         PMG_CUDA(cudaFuncSetAttribute(k_skew<K, NR, C, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        // (GS rows hold the lower half of A's row: <= 61 terms at p = 5)
         PMG_CUDA(cudaFuncSetAttribute(k_skew<K, NR, C, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
         attr = true;
     }
@@ -648,7 +676,11 @@ void skew_sweep(const SkewOp& op, int* ticket, cudaStream_t st) {
         PMG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     }
     const int smem = int(smem_bytes(p.nr, p.dm, p.ry));
-    SkewArgs a{p.item, op.rhs, op.out, p.Db, p.off, p.R, p.W, n, p.seg, p.nseg, p.dm, p.ry, ticket, nullptr};
+    if (op.kind == kSkewGS) {  // upper sums over the old values, before the sweep
+        k_skew_gs_su<<<ceil_div(n, 256), 256, 0, st>>>(*op.gsS, op.nlow, op.old, op.su);
+        PMG_LAUNCH_CHECK();
+    }
+    SkewArgs a{p.item, op.rhs, op.out, p.Db, p.off, p.R, p.W, op.su, n, p.seg, p.nseg, p.dm, p.ry, ticket, nullptr};
     if (g_skew_trace_on) {  // one-shot trace of the next sweep (diagnostics)
         g_skew_trace_on = false;
         cudaFree(g_skew_trace);
@@ -665,7 +697,8 @@ void skew_sweep(const SkewOp& op, int* ticket, cudaStream_t st) {
     const int per_sm = std::max(1, int((227 * 1024) / (smem + 1024)));
     const int grid = std::min(std::min(p.nblk, nsm * per_sm), grid_cap > 0 ? grid_cap : INT_MAX);
     if (op.kind == kSkewL) launch_kind<kSkewL>(p, a, grid, smem, st);
-    else launch_kind<kSkewU>(p, a, grid, smem, st);
+    else if (op.kind == kSkewU) launch_kind<kSkewU>(p, a, grid, smem, st);
+    else launch_kind<kSkewGS>(p, a, grid, smem, st);
     if (op.kind == kSkewU) {
         k_skew_upd<<<ceil_div(n, 256), 256, 0, st>>>(op.out, op.upd, n);
         PMG_LAUNCH_CHECK();

@@ -6,7 +6,7 @@
 
 namespace pmg {
 
-enum SkewKind : int { kSkewL = 0, kSkewU = 1 };
+enum SkewKind : int { kSkewL = 0, kSkewU = 1, kSkewGS = 2 };
 
 // The sweep kernel reads per-(step, lane) items (a lane's stage data, 48 B) stored step-major
 // per warp block, [3 x 16-B chunks][32 lanes] per step, so one bulk copy moves a group of
@@ -33,8 +33,10 @@ struct SkewPlan {
 // (nothing allocated) when a row does not fit: more terms than the widest layout, an entry
 // more than 8 segments back, a term whose value would not be final at its stage, or rings
 // beyond shared memory.
+// Gauss-Seidel (kind kSkewGS): S is the off-diagonal sliced matrix of the sweep (lower entries
+// first, nlow[v] of them), dinv the reciprocal diagonal; the terms are the lower entries.
 bool skew_plan(const Sell& S, const double* dinv, int32_t seg, SkewKind kind, int32_t max_terms, SkewPlan& plan,
-               cudaStream_t st);
+               cudaStream_t st, const int32_t* nlow = nullptr);
 void skew_plan_free(SkewPlan& plan);
 
 struct SkewOp {
@@ -43,6 +45,12 @@ struct SkewOp {
     const double* rhs;   // L: r (natural order); U: y (natural order)
     double* out;         // v-space outputs (sentinel protocol across warp blocks)
     double* upd;         // U: u[i] += x_i after the sweep
+    // Gauss-Seidel: u_new = ((f - S_L) - S_U) / a_ii with S_U over the old values, summed by a
+    // pre-pass (same ascending order as the oracle) into su
+    const Sell* gsS = nullptr;
+    const int32_t* nlow = nullptr;
+    const double* old = nullptr;
+    double* su = nullptr;
 };
 
 void skew_sweep(const SkewOp& op, int* ticket, cudaStream_t st);
