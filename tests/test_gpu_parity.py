@@ -174,3 +174,32 @@ def test_skew_sweeps_cta_loops():
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     res = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True, timeout=600)
     assert res.returncode == 0, res.stderr[-2000:]
+
+
+@pytest.mark.parametrize("p,h_exp", [(1, 5), (2, 6), (3, 6), (4, 6), (5, 6), (5, 7)])
+def test_gs_sweep_skew_degrees(p, h_exp, monkeypatch):
+    """Gauss-Seidel through the skewed-warp kernel (lower entries as stage terms, upper sums over
+    the old values by a pre-pass) on A_p of every degree, bitwise against the oracle's sweep."""
+    monkeypatch.delenv("PMG_SKEW", raising=False)
+    monkeypatch.delenv("PMG_FORCE_LEVELSCHED", raising=False)
+    pb = P.build(P.make_spec(geometry="annulus", rhs="one", degrees=(max(p, 2), 1), h_exp=h_exp))
+    A = pb.hlevels[0].A if p == 1 else pb.plevels[0].A
+    rng = np.random.default_rng(p)
+    u = rng.uniform(-1, 1, A.nrows)
+    f = rng.uniform(-1, 1, A.nrows)
+    assert_bitwise(pmg.gauss_seidel_sweep(A, u, f), O.gauss_seidel_sweep(A, u, f), "gs skew")
+
+
+@pytest.mark.parametrize("p", [2, 3, 4, 5])
+def test_skew_sweeps_long_rows(p, monkeypatch):
+    """The skewed-warp layouts for long rows (8x4, 16x4, 32x3, 32x4 lanes x terms; up to five
+    segments back): ilut_apply on the p-level factor, bitwise against the oracle."""
+    monkeypatch.delenv("PMG_SKEW", raising=False)
+    monkeypatch.delenv("PMG_FORCE_LEVELSCHED", raising=False)
+    pb = P.build(P.make_spec(geometry="annulus", rhs="one", degrees=(p, 1), h_exp=6))
+    A = pb.plevels[0].A
+    Fg = pmg.ilut_factorize(A, 1e-12, 1.0, "none")
+    assert Fg.stats()["sweep"] == "skew"
+    Fo = O.ilut_factorize(A, 1e-12, 1.0, O.ORDER_NONE)
+    r = np.random.default_rng(p).uniform(-1, 1, A.nrows)
+    assert_bitwise(pmg.ilut_apply(Fg, r), Fo.apply(r), "skew ilut_apply")
