@@ -23,6 +23,7 @@
 // Layouts per factor (chosen by skew_plan from the longest row): NR x C = 4 x 3 (p = 1,
 // <= 10 terms), 8 x 4 (<= 29), 16 x 4 (<= 61), 32 x 3 (<= 94), 32 x 4 (<= 125).
 #include <climits>
+#include <cstdio>
 #include <cstdlib>
 #include <vector>
 
@@ -118,6 +119,11 @@ __device__ __forceinline__ void st_rel_cta(int* p, int v) {
     asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
 }
 __device__ __forceinline__ int ld_vol_s(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
+__device__ __forceinline__ void st_shared_if(double* p, double v, bool pred) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.shared.f64 [%0], %1;\n\t}" ::"r"(smem_u32(p)),
+                 "d"(v), "r"(int(pred))
+                 : "memory");
+}
 
 template <int K, int NR, int C, bool TR>
 __global__ void __launch_bounds__(NT) k_skew(SkewArgs a) {
@@ -292,7 +298,6 @@ __global__ void __launch_bounds__(NT) k_skew(SkewArgs a) {
 #pragma unroll
             for (int u = 0; u < G; ++u) {
                 const int t = tb + u;
-                if (t >= NS) break;  // slots past the block's last group hold stale data
                 const int ix = t - P - D * k;  // the segment's stage-0 row at this step
                 if (u == G - 1) group_wait(unsigned(tb) / G + 1);  // for fetch(t + 1) below
                 const double in0 = __shfl_down_sync(FULL, res, 1);  // partial from the next stage's lane
@@ -326,10 +331,11 @@ __global__ void __launch_bounds__(NT) k_skew(SkewArgs a) {
                 const double x = K == kSkewL    ? f.rhs - r1
                                  : K == kSkewU ? (f.rhs - r1) * f.w[1]
                                                : ((f.rhs - r1) - f.su) * f.w[1];  // GS: SPEC order
-                if (role == 0 && ix >= 0 && ix < rows) {
-                    Yo[ix & (RY - 1)] = x;
-                    st_relaxed(a.out + lo + ix, x);
-                    if (TR && a.trace && k == SPW - 1 && ix == 200) a.trace[blk * 8 + 4] = gtimer();
+                {  // predicated stores (no divergent branch on the step's path)
+                    const bool put = role == 0 && ix >= 0 && ix < rows;
+                    st_shared_if(Yo + (ix & (RY - 1)), x, put);
+                    st_relaxed_if(a.out + lo + ix, x, put);
+                    if (TR && a.trace && put && k == SPW - 1 && ix == 200) a.trace[blk * 8 + 4] = gtimer();
                 }
                 xprev = x;
                 if (g0 > 0) hr = ld_vol_s(&sm.halo_ready);  // for the next step's test
@@ -363,7 +369,7 @@ struct RowView {
 // term; returns false if a term does not fit the layout (more than P stages, own value not
 // final by its stage, not ascending, more than MAXD segments back).
 template <int K, class F>
-__device__ bool for_terms(const Sell& S, const int32_t* nlow, int32_t seg, int v, int NR, int C, F&& f) {
+__device__ bool for_terms(const Sell& S, const int32_t* nlow, int32_t seg, int v, int NR, int C, int& why, F&& f) {
     RowView<K> r(S, v, nlow);
     const int g = v / seg, ix = v - g * seg, P = NR - 1;
     int q = r.len - 1;
@@ -372,13 +378,25 @@ __device__ bool for_terms(const Sell& S, const int32_t* nlow, int32_t seg, int v
     bool ok = true;
     for (int b = 0; q >= 0; --q, ++b) {
         const int c = r.col(q);
-        if (c >= prev || c >= v) ok = false;  // terms must be strictly ascending and below v
+        if (c >= prev || c >= v) {  // terms must be strictly ascending and below v
+            ok = false;
+            why |= 1;
+        }
         prev = c;
         const int st = 1 + b / C;
-        if (st > P) return false;
+        if (st > P) {
+            why |= 2;
+            return false;
+        }
         const int gc = c / seg, jx = c - gc * seg, d = g - gc;
-        if (d == 0 && st > ix - jx - 1) ok = false;  // own value not final by the stage's step
-        if (d > MAXD) return false;
+        if (d == 0 && st > ix - jx - 1) {  // own value not final by the stage's step
+            ok = false;
+            why |= 4;
+        }
+        if (d > MAXD) {
+            why |= 8;
+            return false;
+        }
         f(st, d, jx, ix);
     }
     return ok;
@@ -391,8 +409,8 @@ __global__ void k_skew_req(Sell S, const int32_t* nlow, int32_t seg, int NR, int
     const int32_t v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= S.n) return;
     const int SPW = 32 / NR, g = v / seg, k = g % SPW;
-    int dreq = 1, back0 = INT_MIN, dmax = 0;
-    const bool ok = for_terms<K>(S, nlow, seg, v, NR, C, [&](int st, int d, int jx, int ix) {
+    int dreq = 1, back0 = INT_MIN, dmax = 0, why = 0;
+    const bool ok = for_terms<K>(S, nlow, seg, v, NR, C, why, [&](int st, int d, int jx, int ix) {
         if (d == 0) {
             back0 = max(back0, ix - jx - st);
         } else {
@@ -402,7 +420,7 @@ __global__ void k_skew_req(Sell S, const int32_t* nlow, int32_t seg, int NR, int
         }
     });
     atomicMax(Db + g / SPW, dreq);
-    if (!ok) atomicMax(out + 0, 1);
+    if (!ok) atomicOr(out + 0, why | 16);
     atomicMax(out + 1, back0);
     atomicMax(out + 2, dmax);
 }
@@ -419,7 +437,8 @@ __global__ void k_skew_req2(Sell S, const int32_t* nlow, int32_t seg, int NR, in
     int ring = INT_MIN;
     int Rl[MAXD], Wl[MAXD];
     for (int d = 0; d < MAXD; ++d) Rl[d] = Wl[d] = INT_MIN;
-    for_terms<K>(S, nlow, seg, v, NR, C, [&](int st, int d, int jx, int ix) {
+    int why = 0;
+    for_terms<K>(S, nlow, seg, v, NR, C, why, [&](int st, int d, int jx, int ix) {
         if (d == 0) return;
         if (d <= k) {
             ring = max(ring, ix - jx - st + d * D);  // writer row at the read minus jx
@@ -573,7 +592,13 @@ bool skew_plan(const Sell& S, const double* dinv, int32_t seg, SkewKind kind, in
     PMG_CUDA(cudaMemcpyAsync(hR.data(), R, sizeof(int32_t) * hR.size(), cudaMemcpyDeviceToHost, st));
     PMG_CUDA(cudaMemcpyAsync(hW.data(), W, sizeof(int32_t) * hW.size(), cudaMemcpyDeviceToHost, st));
     PMG_CUDA(cudaStreamSynchronize(st));
-    if (h[0]) return fail();
+    if (h[0]) {
+        if (getenv("PMG_VERBOSE"))
+            fprintf(stderr, "[pmg] skew plan rejected (n=%d seg=%d NR=%d): %s%s%s%s\n", S.n, seg, NR,
+                    h[0] & 1 ? "unsorted " : "", h[0] & 2 ? "row too long " : "", h[0] & 4 ? "own value late " : "",
+                    h[0] & 8 ? "term > 8 segments back" : "");
+        return fail();
+    }
     const int dm = std::max(h[2], 1);
     // rings: the own segment's back reach, what a reader inside the block still needs, and
     // the halo window (lead + read-behind) with room for the bridge to run ahead
@@ -591,7 +616,9 @@ bool skew_plan(const Sell& S, const double* dinv, int32_t seg, SkewKind kind, in
     std::vector<int64_t> hoff(nblk + 1, 0);
     for (int b = 0; b < nblk; ++b) {
         const int kl = std::min(SPW - 1, nseg - 1 - b * SPW);
-        hoff[b + 1] = hoff[b] + seg + int64_t(kl) * hD[b] + P;
+        // whole bulk-copy groups: the padding steps hold rows past the segments (zero items)
+        const int64_t ns = seg + int64_t(kl) * hD[b] + P;
+        hoff[b + 1] = hoff[b] + (ns + G - 1) / G * G;
     }
     const int64_t nsteps = hoff[nblk];
     PMG_CUDA(cudaMemcpyAsync(off, hoff.data(), sizeof(int64_t) * (nblk + 1), cudaMemcpyHostToDevice, st));
