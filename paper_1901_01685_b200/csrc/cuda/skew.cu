@@ -25,6 +25,7 @@
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 #include <vector>
 
 #include "skew.cuh"
@@ -76,6 +77,10 @@ struct SkewArgs {
     const int32_t* R;         // [nblk][MAXD] lead (rows) a halo segment needs over segment 0
     const int32_t* W;         // [nblk][MAXD] how far behind segment 0 a halo value is still read
     const double* su;         // Gauss-Seidel upper sums (natural order)
+    const int32_t* far_off;   // [nblk+1] far-table entries of the block (terms > MAXD segments back)
+    const int32_t* far_idx;   // v-space rows of those values, sorted per block
+    const int32_t* far_blk;   // [nblk] the last block the far values come from (-1: none)
+    int* done;                // [nblk] block finished (release), reset per sweep
     int32_t n, seg, nseg, dm, ry;
     int* ticket;
     unsigned long long* trace;  // optional: per block [claim, end, halo wait cycles, bridge polls, ...]
@@ -189,6 +194,18 @@ __global__ void __launch_bounds__(NT) k_skew(SkewArgs a) {
             // the previous block's last DM segments -> halo rings, in order, as values appear.
             // halo_ready = h publishes [0, h + (delta-1)*D) of segment g0-delta for every delta.
             if (g0 > 0) {
+                const int f0 = a.far_off[blk], nf = a.far_off[blk + 1] - f0;
+                if (nf > 0) {  // far values: once their last block is done, copy them once
+                    const int* dn = a.done + a.far_blk[blk];
+                    unsigned ns = 64;
+                    while (ld_acquire(dn) == 0) {
+                        __nanosleep(ns);
+                        ns = min(ns * 2, 1024u);
+                    }
+                    double* far = Ybase + (DM + SPW) * RYS;
+                    for (int i = lane; i < nf; i += 32) far[i] = a.out[a.far_idx[f0 + i]];
+                    __syncwarp();
+                }
                 int f[MAXD], Rq[MAXD], Wq[MAXD];
 #pragma unroll
                 for (int d = 0; d < MAXD; ++d) {
@@ -348,6 +365,11 @@ __global__ void __launch_bounds__(NT) k_skew(SkewArgs a) {
             refill(qd + NG);
         }
         if (TR && a.trace && lane == 0) a.trace[blk * 8 + 1] = gtimer();
+        __syncwarp();  // every row of the block is stored: publish (blocks far ahead read it)
+        if (lane == 0) {
+            __threadfence();
+            st_release(a.done + blk, 1);
+        }
     }
 }
 
@@ -393,11 +415,7 @@ __device__ bool for_terms(const Sell& S, const int32_t* nlow, int32_t seg, int v
             ok = false;
             why |= 4;
         }
-        if (d > MAXD) {
-            why |= 8;
-            return false;
-        }
-        f(st, d, jx, ix);
+        f(st, d, jx, ix, c);  // d > MAXD: a "far" term, read from the block's far table
     }
     return ok;
 }
@@ -405,14 +423,18 @@ __device__ bool for_terms(const Sell& S, const int32_t* nlow, int32_t seg, int v
 // pass 1a: per block, the lane skew D_b covering every term inside the block; global failure,
 // own-segment back reach and segments-back reach.  out[0] fail, out[1] back0, out[2] dmax
 template <int K>
-__global__ void k_skew_req(Sell S, const int32_t* nlow, int32_t seg, int NR, int C, int32_t* Db, int* out) {
+__global__ void k_skew_req(Sell S, const int32_t* nlow, int32_t seg, int NR, int C, int32_t* Db, int* out,
+                           int* nfar, uint64_t* far, int far_cap) {
     const int32_t v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= S.n) return;
     const int SPW = 32 / NR, g = v / seg, k = g % SPW;
     int dreq = 1, back0 = INT_MIN, dmax = 0, why = 0;
-    const bool ok = for_terms<K>(S, nlow, seg, v, NR, C, why, [&](int st, int d, int jx, int ix) {
+    const bool ok = for_terms<K>(S, nlow, seg, v, NR, C, why, [&](int st, int d, int jx, int ix, int c) {
         if (d == 0) {
             back0 = max(back0, ix - jx - st);
+        } else if (d > MAXD) {
+            const int i = atomicAdd(nfar, 1);  // (block, column) of a far term
+            if (far && i < far_cap) far[i] = (uint64_t(uint32_t(g / SPW)) << 32) | uint32_t(c);
         } else {
             dmax = max(dmax, d);
             const int need = st + 1 + jx - ix;  // d * D >= need for a term inside the block
@@ -438,8 +460,8 @@ __global__ void k_skew_req2(Sell S, const int32_t* nlow, int32_t seg, int NR, in
     int Rl[MAXD], Wl[MAXD];
     for (int d = 0; d < MAXD; ++d) Rl[d] = Wl[d] = INT_MIN;
     int why = 0;
-    for_terms<K>(S, nlow, seg, v, NR, C, why, [&](int st, int d, int jx, int ix) {
-        if (d == 0) return;
+    for_terms<K>(S, nlow, seg, v, NR, C, why, [&](int st, int d, int jx, int ix, int) {
+        if (d == 0 || d > MAXD) return;
         if (d <= k) {
             ring = max(ring, ix - jx - st + d * D);  // writer row at the read minus jx
         } else {
@@ -459,7 +481,7 @@ __global__ void k_skew_req2(Sell S, const int32_t* nlow, int32_t seg, int NR, in
 // pass 2: step-major items, one thread per (step, lane)
 template <int K>
 __global__ void k_skew_fill(Sell S, const int32_t* __restrict__ nlow, const double* __restrict__ dinv, int32_t seg,
-                            int32_t nseg,
+                            int32_t nseg, const int32_t* __restrict__ far_off, const int32_t* __restrict__ far_idx,
                             const int32_t* __restrict__ Db, const int64_t* __restrict__ off, int32_t nblk, int NR,
                             int C, int RY, int64_t nsteps, uint4* __restrict__ item) {
     const int64_t gid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -499,7 +521,17 @@ __global__ void k_skew_fill(Sell S, const int32_t* __restrict__ nlow, const doub
                 const int c = r.col(kk);
                 const int gc = c / seg, jx = c - gc * seg, d = g - gc;
                 it.w[C - 1 - s] = r.val(kk);
-                it.o[C - 1 - s] = (-d * RYS + (jx & (RY - 1))) * 8;
+                if (d <= MAXD) {
+                    it.o[C - 1 - s] = (-d * RYS + (jx & (RY - 1))) * 8;
+                } else {  // far table after the block's rings: slot of c in the block's sorted list
+                    int lo2 = far_off[b], hi2 = far_off[b + 1];
+                    while (lo2 < hi2) {
+                        const int mid = (lo2 + hi2) >> 1;
+                        if (far_idx[mid] < c) lo2 = mid + 1;
+                        else hi2 = mid;
+                    }
+                    it.o[C - 1 - s] = ((SPW - k) * RYS + (lo2 - far_off[b])) * 8;
+                }
             }
         }
     }
@@ -529,7 +561,9 @@ __global__ void k_skew_upd(const double* __restrict__ x, double* __restrict__ u,
     u[i] = u[i] + x[v];
 }
 
-size_t smem_bytes(int NR, int dm, int ry) { return sizeof(SkewSmem) + sizeof(double) * (dm + 32 / NR) * (ry + 1); }
+size_t smem_bytes(int NR, int dm, int ry, int nfar) {
+    return sizeof(SkewSmem) + sizeof(double) * ((dm + 32 / NR) * (ry + 1) + nfar);
+}
 
 }  // namespace
 
@@ -577,10 +611,51 @@ bool skew_plan(const Sell& S, const double* dinv, int32_t seg, SkewKind kind, in
     const int init[4] = {0, INT_MIN, 0, INT_MIN};
     PMG_CUDA(cudaMemcpyAsync(d, init, sizeof(init), cudaMemcpyHostToDevice, st));
     const int nb = ceil_div(S.n, 256);
-    if (kind == kSkewL) k_skew_req<kSkewL><<<nb, 256, 0, st>>>(S, nlow, seg, NR, C, Db, d);
-    else if (kind == kSkewU) k_skew_req<kSkewU><<<nb, 256, 0, st>>>(S, nlow, seg, NR, C, Db, d);
-    else k_skew_req<kSkewGS><<<nb, 256, 0, st>>>(S, nlow, seg, NR, C, Db, d);
-    PMG_LAUNCH_CHECK();
+    // far terms (> MAXD segments back, e.g. patch interfaces): counted, then collected
+    int* nfar = nullptr;
+    uint64_t* farp = nullptr;
+    PMG_CUDA(cudaMalloc(&nfar, sizeof(int)));
+    auto req = [&](uint64_t* fp, int cap) {
+        PMG_CUDA(cudaMemsetAsync(nfar, 0, sizeof(int), st));
+        PMG_CUDA(cudaMemsetAsync(Db, 0, sizeof(int32_t) * nblk, st));
+        if (kind == kSkewL) k_skew_req<kSkewL><<<nb, 256, 0, st>>>(S, nlow, seg, NR, C, Db, d, nfar, fp, cap);
+        else if (kind == kSkewU) k_skew_req<kSkewU><<<nb, 256, 0, st>>>(S, nlow, seg, NR, C, Db, d, nfar, fp, cap);
+        else k_skew_req<kSkewGS><<<nb, 256, 0, st>>>(S, nlow, seg, NR, C, Db, d, nfar, fp, cap);
+        PMG_LAUNCH_CHECK();
+        int h = 0;
+        PMG_CUDA(cudaMemcpyAsync(&h, nfar, sizeof(int), cudaMemcpyDeviceToHost, st));
+        PMG_CUDA(cudaStreamSynchronize(st));
+        return h;
+    };
+    const int nfar_terms = req(nullptr, 0);
+    std::vector<uint64_t> hfar;
+    if (nfar_terms > 0) {
+        PMG_CUDA(cudaMalloc(&farp, sizeof(uint64_t) * nfar_terms));
+        req(farp, nfar_terms);
+        hfar.resize(nfar_terms);
+        PMG_CUDA(cudaMemcpy(hfar.data(), farp, sizeof(uint64_t) * nfar_terms, cudaMemcpyDeviceToHost));
+        cudaFree(farp);
+    }
+    cudaFree(nfar);
+    // per block: sorted distinct far rows and the last block they come from
+    std::sort(hfar.begin(), hfar.end());
+    hfar.erase(std::unique(hfar.begin(), hfar.end()), hfar.end());
+    std::vector<int32_t> hfo(nblk + 1, 0), hfi, hfb(nblk, -1);
+    int max_far = 0;
+    {
+        size_t q = 0;
+        for (int b = 0; b < nblk; ++b) {
+            hfo[b] = int32_t(hfi.size());
+            while (q < hfar.size() && int(hfar[q] >> 32) == b) {
+                const int32_t c = int32_t(uint32_t(hfar[q]));
+                hfi.push_back(c);
+                hfb[b] = std::max(hfb[b], (c / seg) / SPW);
+                ++q;
+            }
+            max_far = std::max(max_far, int(hfi.size()) - hfo[b]);
+        }
+        hfo[nblk] = int32_t(hfi.size());
+    }
     if (kind == kSkewL) k_skew_req2<kSkewL><<<nb, 256, 0, st>>>(S, nlow, seg, NR, C, Db, R, W, d + 3);
     else if (kind == kSkewU) k_skew_req2<kSkewU><<<nb, 256, 0, st>>>(S, nlow, seg, NR, C, Db, R, W, d + 3);
     else k_skew_req2<kSkewGS><<<nb, 256, 0, st>>>(S, nlow, seg, NR, C, Db, R, W, d + 3);
@@ -612,7 +687,17 @@ bool skew_plan(const Sell& S, const double* dinv, int32_t seg, SkewKind kind, in
     }
     int ry = 64;
     while (ry <= need) ry *= 2;
-    if (ry > 1024 || smem_bytes(NR, dm, ry) > 227 * 1024) return fail();
+    if (ry > 1024 || smem_bytes(NR, dm, ry, max_far) > 227 * 1024) return fail();
+    int32_t *far_off = nullptr, *far_idx = nullptr, *far_blk = nullptr;
+    int* done = nullptr;
+    PMG_CUDA(cudaMalloc(&far_off, sizeof(int32_t) * (nblk + 1)));
+    PMG_CUDA(cudaMalloc(&far_idx, sizeof(int32_t) * std::max<size_t>(hfi.size(), 1)));
+    PMG_CUDA(cudaMalloc(&far_blk, sizeof(int32_t) * nblk));
+    PMG_CUDA(cudaMalloc(&done, sizeof(int) * nblk));
+    PMG_CUDA(cudaMemcpyAsync(far_off, hfo.data(), sizeof(int32_t) * (nblk + 1), cudaMemcpyHostToDevice, st));
+    if (!hfi.empty())
+        PMG_CUDA(cudaMemcpyAsync(far_idx, hfi.data(), sizeof(int32_t) * hfi.size(), cudaMemcpyHostToDevice, st));
+    PMG_CUDA(cudaMemcpyAsync(far_blk, hfb.data(), sizeof(int32_t) * nblk, cudaMemcpyHostToDevice, st));
     std::vector<int64_t> hoff(nblk + 1, 0);
     for (int b = 0; b < nblk; ++b) {
         const int kl = std::min(SPW - 1, nseg - 1 - b * SPW);
@@ -627,11 +712,14 @@ bool skew_plan(const Sell& S, const double* dinv, int32_t seg, SkewKind kind, in
     const int64_t nthr = nsteps * 32;
     const int nf = ceil_div(nthr, 256);
     if (kind == kSkewL)
-        k_skew_fill<kSkewL><<<nf, 256, 0, st>>>(S, nlow, dinv, seg, nseg, Db, off, nblk, NR, C, ry, nsteps, item);
+        k_skew_fill<kSkewL><<<nf, 256, 0, st>>>(S, nlow, dinv, seg, nseg, far_off, far_idx, Db, off, nblk, NR, C, ry,
+                                                nsteps, item);
     else if (kind == kSkewU)
-        k_skew_fill<kSkewU><<<nf, 256, 0, st>>>(S, nlow, dinv, seg, nseg, Db, off, nblk, NR, C, ry, nsteps, item);
+        k_skew_fill<kSkewU><<<nf, 256, 0, st>>>(S, nlow, dinv, seg, nseg, far_off, far_idx, Db, off, nblk, NR, C, ry,
+                                                nsteps, item);
     else
-        k_skew_fill<kSkewGS><<<nf, 256, 0, st>>>(S, nlow, dinv, seg, nseg, Db, off, nblk, NR, C, ry, nsteps, item);
+        k_skew_fill<kSkewGS><<<nf, 256, 0, st>>>(S, nlow, dinv, seg, nseg, far_off, far_idx, Db, off, nblk, NR, C,
+                                                 ry, nsteps, item);
     PMG_LAUNCH_CHECK();
     PMG_CUDA(cudaStreamSynchronize(st));
     cudaFree(d);
@@ -653,12 +741,21 @@ bool skew_plan(const Sell& S, const double* dinv, int32_t seg, SkewKind kind, in
     plan.R = R;
     plan.W = W;
     plan.item = item;
+    plan.far_off = far_off;
+    plan.far_idx = far_idx;
+    plan.far_blk = far_blk;
+    plan.done = done;
+    plan.nfar_max = max_far;
     plan.ok = true;
     return true;
 }
 
 void skew_plan_free(SkewPlan& plan) {
     cudaFree(plan.item);
+    cudaFree(plan.far_off);
+    cudaFree(plan.far_idx);
+    cudaFree(plan.far_blk);
+    cudaFree(plan.done);
     cudaFree(plan.Db);
     cudaFree(plan.off);
     cudaFree(plan.R);
@@ -702,12 +799,14 @@ void skew_sweep(const SkewOp& op, int* ticket, cudaStream_t st) {
         PMG_CUDA(cudaGetDevice(&dev));
         PMG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     }
-    const int smem = int(smem_bytes(p.nr, p.dm, p.ry));
+    const int smem = int(smem_bytes(p.nr, p.dm, p.ry, p.nfar_max));
+    PMG_CUDA(cudaMemsetAsync(p.done, 0, sizeof(int) * p.nblk, st));
     if (op.kind == kSkewGS) {  // upper sums over the old values, before the sweep
         k_skew_gs_su<<<ceil_div(n, 256), 256, 0, st>>>(*op.gsS, op.nlow, op.old, op.su);
         PMG_LAUNCH_CHECK();
     }
-    SkewArgs a{p.item, op.rhs, op.out, p.Db, p.off, p.R, p.W, op.su, n, p.seg, p.nseg, p.dm, p.ry, ticket, nullptr};
+    SkewArgs a{p.item,    op.rhs,    op.out,    p.Db,   p.off, p.R,   p.W,   op.su,   p.far_off, p.far_idx,
+               p.far_blk, p.done,    n,         p.seg,  p.nseg, p.dm, p.ry, ticket, nullptr};
     if (g_skew_trace_on) {  // one-shot trace of the next sweep (diagnostics)
         g_skew_trace_on = false;
         cudaFree(g_skew_trace);

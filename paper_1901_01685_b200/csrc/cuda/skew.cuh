@@ -25,6 +25,13 @@ struct SkewPlan {
     int32_t* R = nullptr;      // [nblk][8] lead a halo segment needs over the block's segment 0
     int32_t* W = nullptr;      // [nblk][8] read-behind window of the halo rings
     uint4* item = nullptr;     // [nsteps][3][32]
+    // terms more than 8 segments back (patch interfaces): per block a table of those values,
+    // copied once their last block is done
+    int32_t* far_off = nullptr;  // [nblk+1]
+    int32_t* far_idx = nullptr;  // sorted v-space rows per block
+    int32_t* far_blk = nullptr;  // [nblk] block the last far value comes from (-1: none)
+    int* done = nullptr;         // [nblk] finished blocks of the current sweep
+    int32_t nfar_max = 0;
     bool ok = false;
 };
 
