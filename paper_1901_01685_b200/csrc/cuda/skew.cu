@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(NT) k_skew(SkewArgs a) {
                     if (moved) {  // spin while values flow (this warp has its own scheduler slot)
                         ns = 16;
                         idle = 0;
-                    } else if (++idle > 8) {
+                    } else if (++idle > 8 && pub >= cons) {  // sleep only while segment 0 is not waiting
                         __nanosleep(ns);
                         ns = min(ns * 2, 256u);
                     }
