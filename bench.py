@@ -278,6 +278,14 @@ def main():
         r_ach = ab["resid_fine"] / (r_ms * 1e-3) / 1e9
         roof["spmv_residual"] = {"achieved": r_ach, "frac": r_ach / peak, "ms_per_launch": r_ms,
                                  "bytes_per_launch": ab["resid_fine"]}
+    # every fine-level kernel class against the same roofline (algorithmic bytes / class time)
+    per_kernel = {}
+    for k2, nops in (("resid_fine", 1), ("lsolve_fine", 3), ("usolve_fine", 3), ("gs_fine", 3), ("transfer", 2)):
+        if la.get(k2, 0) > 0 and k2 in ab:
+            ms_op = ms[k2] / (la[k2] / nops)
+            gbs = ab[k2] / (ms_op * 1e-3) / 1e9
+            per_kernel[k2] = {"ms": ms_op, "bytes": ab[k2], "achieved_GBs": gbs, "frac": gbs / peak}
+    roof["per_kernel"] = per_kernel
     # per-V-cycle aggregate fraction
     total_bytes_cycle = ab["resid_fine"] * 3 + ab.get("transfer", 0)
     if "lsolve_fine" in ab:
