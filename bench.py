@@ -255,14 +255,12 @@ def main():
     ms, la = kt["ms"], kt["launches_by_class"]
     cands = {k: ms[k] for k in ("resid_fine", "lsolve_fine", "usolve_fine", "gs_fine", "transfer") if la.get(k, 0) > 0}
     dom = max(cands, key=cands.get)
-    per_launch_ms = ms[dom] / la[dom]
-    launches_dom = la[dom]
-    if dom in ("lsolve_fine", "usolve_fine", "gs_fine"):
-        per_launch_ms = ms[dom] / (la[dom] / 3)  # sentinel fill + ticket reset + sweep = one operation
-        launches_dom = la[dom] // 3
-    elif dom == "transfer":
-        per_launch_ms = ms[dom] / (la[dom] / 2)
-        launches_dom = la[dom] // 2
+    # operations in the timed region: a sweep class runs nu1 + nu2 = 2 sweeps per V-cycle (each a
+    # few launches: sentinel fill, sweep, U update), the transfers one restrict + prolong per cycle
+    nops = {"resid_fine": la.get("resid_fine", 0), "lsolve_fine": 2 * cycles, "usolve_fine": 2 * cycles,
+            "gs_fine": 2 * cycles, "transfer": cycles}
+    per_launch_ms = ms[dom] / max(nops[dom], 1)
+    launches_dom = nops[dom]
     bytes_dom = ab[dom]
     achieved = bytes_dom / (per_launch_ms * 1e-3) / 1e9
     peak, peak_kind = peaks()
@@ -280,9 +278,9 @@ def main():
                                  "bytes_per_launch": ab["resid_fine"]}
     # every fine-level kernel class against the same roofline (algorithmic bytes / class time)
     per_kernel = {}
-    for k2, nops in (("resid_fine", 1), ("lsolve_fine", 3), ("usolve_fine", 3), ("gs_fine", 3), ("transfer", 2)):
+    for k2 in ("resid_fine", "lsolve_fine", "usolve_fine", "gs_fine", "transfer"):
         if la.get(k2, 0) > 0 and k2 in ab:
-            ms_op = ms[k2] / (la[k2] / nops)
+            ms_op = ms[k2] / max(nops[k2], 1)
             gbs = ab[k2] / (ms_op * 1e-3) / 1e9
             per_kernel[k2] = {"ms": ms_op, "bytes": ab[k2], "achieved_GBs": gbs, "frac": gbs / peak}
     roof["per_kernel"] = per_kernel

@@ -529,17 +529,18 @@ void smooth_ilut(pmg_work_s& W, pmg_csr_s* A, pmg_factor_s* F, double* u, const 
         W.run(fine ? kClsResid0 : kClsCoarse, 1, [&] { sell_rowop(A->S, kOpResidual, u, f, nullptr, r, nullptr, W.st); });
         rr = r;
     }
+    // launch counts: our kernels per sweep (sentinel fill, sweep, and the U update pass)
     if (F->skew) {
-        W.run(fine ? kClsL0 : kClsCoarse, 4, [&] {
+        W.run(fine ? kClsL0 : kClsCoarse, 2, [&] {
             SkewOp l{kSkewL, &F->planL, rr, y, nullptr};
             skew_sweep(l, W.ticket, W.st);
         });
-        W.run(fine ? kClsU0 : kClsCoarse, 4, [&] {
+        W.run(fine ? kClsU0 : kClsCoarse, 3, [&] {
             SkewOp up{kSkewU, &F->planU, y, x, u};
             skew_sweep(up, W.ticket, W.st);
         });
     } else if (F->seg > 0) {
-        W.run(fine ? kClsL0 : kClsCoarse, 3, [&] {
+        W.run(fine ? kClsL0 : kClsCoarse, 2, [&] {
             ChainOp l{kChainL, &F->Ls, nullptr, nullptr, F->splitL, F->perm, rr, nullptr, y, nullptr, F->seg, F->bs, F->gapL};
             chain_sweep(l, W.ticket, W.st);
         });
@@ -582,7 +583,7 @@ int smooth(pmg_work_s& W, int l, const double* f, const double* r_known) {
         if (L.A->gs_zero_row >= 0) return PMG_ZERO_DIAG;
         double* uo = w.u[w.cur];
         double* un = w.u[1 - w.cur];
-        W.run(fine ? kClsGS0 : kClsCoarse, 3, [&] { gs_apply(L.A, f, uo, un, W.ticket, W.st); });
+        W.run(fine ? kClsGS0 : kClsCoarse, L.A->gs_skew ? 3 : 2, [&] { gs_apply(L.A, f, uo, un, W.ticket, W.st); });
         w.cur = 1 - w.cur;
         return PMG_OK;
     }
