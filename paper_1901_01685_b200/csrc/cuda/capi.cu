@@ -122,7 +122,6 @@ struct pmg_csr_s {
     bool gs_chain = false;        // chained GS sweep (else level-scheduled)
     bool gs_skew = false;         // skewed-warp GS sweep (default for tensor-grid orderings)
     SkewPlan gs_plan;
-    double* gs_su = nullptr;      // upper sums over the old values (skew GS pre-pass)
     ~pmg_csr_s() {
         A.free();
         sell_free(S);
@@ -133,7 +132,6 @@ struct pmg_csr_s {
             cudaFree(gs_nlow);
             cudaFree(gs_split);
             skew_plan_free(gs_plan);
-            cudaFree(gs_su);
         }
     }
 };
@@ -192,9 +190,11 @@ void apply_factor(pmg_factor_s* F, const double* r, double* y, double* x, double
     }
 }
 
-void gs_apply(pmg_csr_s* A, const double* f, const double* uo, double* un, int* ticket, cudaStream_t st) {
+// su: n doubles of caller scratch (the skew pre-pass writes the upper sums there)
+void gs_apply(pmg_csr_s* A, const double* f, const double* uo, double* un, double* su, int* ticket,
+              cudaStream_t st) {
     if (A->gs_skew) {
-        SkewOp g{kSkewGS, &A->gs_plan, f, un, nullptr, &A->gs, A->gs_nlow, uo, A->gs_su};
+        SkewOp g{kSkewGS, &A->gs_plan, f, un, nullptr, &A->gs, A->gs_nlow, uo, su};
         skew_sweep(g, ticket, st);
     } else if (A->gs_chain) {
         ChainOp g{kChainGS, &A->gs, A->gs_diag, A->gs_nlow, A->gs_split, nullptr, f, uo, un, nullptr, A->seg, 8, A->gs_gap};
@@ -261,7 +261,6 @@ void ensure_gs(pmg_csr_s* h, cudaStream_t st) {
         int32_t mx = 0;
         for (int32_t v : nl) mx = std::max(mx, v);
         h->gs_skew = skew_plan(h->gs, h->gs_diag, h->seg, kSkewGS, mx, h->gs_plan, st, h->gs_nlow);
-        if (h->gs_skew) h->gs_su = dalloc<double>(n);
     }
     h->gs_ready = true;
 }
@@ -583,7 +582,8 @@ int smooth(pmg_work_s& W, int l, const double* f, const double* r_known) {
         if (L.A->gs_zero_row >= 0) return PMG_ZERO_DIAG;
         double* uo = w.u[w.cur];
         double* un = w.u[1 - w.cur];
-        W.run(fine ? kClsGS0 : kClsCoarse, L.A->gs_skew ? 3 : 2, [&] { gs_apply(L.A, f, uo, un, W.ticket, W.st); });
+        W.run(fine ? kClsGS0 : kClsCoarse, L.A->gs_skew ? 3 : 2,
+              [&] { gs_apply(L.A, f, uo, un, w.y, W.ticket, W.st); });  // w.y: idle in GS mode
         w.cur = 1 - w.cur;
         return PMG_OK;
     }
@@ -939,10 +939,11 @@ int pmg_gs_sweep(pmg_csr A, double* u, const double* f, int64_t* err_row) {
         double* du = hv.make(n);
         double* dn = hv.make(n);
         double* df = hv.make(n);
-        int* tk = reinterpret_cast<int*>(hv.make(1));
+        double* dsu = hv.make(n);
+        int* tk = reinterpret_cast<int*>(hv.make(kSweepScratchInts / 2));  // ticket + per-sweep scratch
         PMG_CUDA(cudaMemcpyAsync(du, u, sizeof(double) * n, cudaMemcpyHostToDevice, s.s));
         PMG_CUDA(cudaMemcpyAsync(df, f, sizeof(double) * n, cudaMemcpyHostToDevice, s.s));
-        gs_apply(A, df, du, dn, tk, s.s);
+        gs_apply(A, df, du, dn, dsu, tk, s.s);
         PMG_CUDA(cudaMemcpyAsync(u, dn, sizeof(double) * n, cudaMemcpyDeviceToHost, s.s));
         PMG_CUDA(cudaStreamSynchronize(s.s));
         return int(PMG_OK);
@@ -979,7 +980,7 @@ int pmg_ilut_apply(pmg_factor F, const double* r, double* e) {
         double* dy = hv.make(n);
         double* dx = hv.make(n);
         double* de = hv.make(n);
-        int* tk = reinterpret_cast<int*>(hv.make(1));
+        int* tk = reinterpret_cast<int*>(hv.make(kSweepScratchInts / 2));  // ticket + per-sweep scratch
         PMG_CUDA(cudaMemcpyAsync(dr, r, sizeof(double) * n, cudaMemcpyHostToDevice, s.s));
         PMG_CUDA(cudaMemsetAsync(de, 0, sizeof(double) * n, s.s));
         apply_factor(F, dr, dy, dx, de, tk, s.s);
@@ -1168,7 +1169,7 @@ int pmg_work_create(pmg_hier H, pmg_work* out) {
             w.y = dalloc<double>(n);
             w.x = dalloc<double>(n);
         }
-        W->ticket = reinterpret_cast<int*>(dalloc<double>(1));
+        W->ticket = reinterpret_cast<int*>(dalloc<double>(kSweepScratchInts / 2));  // ticket + per-sweep scratch
         const int32_t n0 = H->pl[0].A->A.n;
         W->nc.partials = dalloc<double>(ceil_div(n0, 256) + 1);
         W->nc.counter = reinterpret_cast<unsigned*>(dalloc<double>(1));

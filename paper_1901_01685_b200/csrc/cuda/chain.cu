@@ -592,12 +592,18 @@ void chain_sweep(const ChainOp& op, int* ticket, cudaStream_t st) {
     fill_sentinel(op.out, n, st);
     PMG_CUDA(cudaMemsetAsync(ticket, 0, sizeof(int), st));
     const int nseg = ceil_div(n, op.seg);
-    static int* prog = nullptr;
-    static int prog_cap = 0;
-    if (nseg > prog_cap) {
-        cudaFree(prog);
-        PMG_CUDA(cudaMalloc(&prog, sizeof(int) * nseg));
-        prog_cap = nseg;
+    // segment progress: the caller's scratch after the ticket (one shared spill buffer only for
+    // orderings with more segments than the scratch holds)
+    static int* spill = nullptr;
+    static int spill_cap = 0;
+    int* prog = ticket + 1;
+    if (nseg >= kSweepScratchInts) {
+        if (nseg > spill_cap) {
+            cudaFree(spill);
+            PMG_CUDA(cudaMalloc(&spill, sizeof(int) * nseg));
+            spill_cap = nseg;
+        }
+        prog = spill;
     }
     PMG_CUDA(cudaMemsetAsync(prog, 0, sizeof(int) * nseg, st));
     static int ahead = -1, gap = -1;

@@ -67,6 +67,11 @@ void vec_norm(const double* v, int32_t n, const NormCtx& ctx, cudaStream_t st);
 void vec_dot(const double* x, const double* y, int32_t n, NormCtx ctx, cudaStream_t st);
 
 void fill_value(double* v, int64_t n, double value_bits_as_double, cudaStream_t st);
+
+// every sweep receives `ticket`: ticket[0] is the CTA claim counter, ticket[1 .. kSweepScratchInts)
+// per-sweep scratch (segment progress / finished blocks) owned by the caller's work object, so
+// concurrent solves on one hierarchy never share it
+constexpr int kSweepScratchInts = 1 << 17;
 void fill_sentinel(double* v, int64_t n, cudaStream_t st);
 
 }  // namespace pmg

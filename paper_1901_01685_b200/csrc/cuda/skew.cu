@@ -800,13 +800,16 @@ void skew_sweep(const SkewOp& op, int* ticket, cudaStream_t st) {
         PMG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     }
     const int smem = int(smem_bytes(p.nr, p.dm, p.ry, p.nfar_max));
-    PMG_CUDA(cudaMemsetAsync(p.done, 0, sizeof(int) * p.nblk, st));
+    // finished-block flags: the caller's scratch after the ticket (the plan's own array only for
+    // factors with more blocks than the scratch holds)
+    int* done = p.nblk < kSweepScratchInts ? ticket + 1 : p.done;
+    PMG_CUDA(cudaMemsetAsync(done, 0, sizeof(int) * p.nblk, st));
     if (op.kind == kSkewGS) {  // upper sums over the old values, before the sweep
         k_skew_gs_su<<<ceil_div(n, 256), 256, 0, st>>>(*op.gsS, op.nlow, op.old, op.su);
         PMG_LAUNCH_CHECK();
     }
     SkewArgs a{p.item,    op.rhs,    op.out,    p.Db,   p.off, p.R,   p.W,   op.su,   p.far_off, p.far_idx,
-               p.far_blk, p.done,    n,         p.seg,  p.nseg, p.dm, p.ry, ticket, nullptr};
+               p.far_blk, done,      n,         p.seg,  p.nseg, p.dm, p.ry, ticket, nullptr};
     if (g_skew_trace_on) {  // one-shot trace of the next sweep (diagnostics)
         g_skew_trace_on = false;
         cudaFree(g_skew_trace);
