@@ -203,3 +203,42 @@ def test_skew_sweeps_long_rows(p, monkeypatch):
     Fo = O.ilut_factorize(A, 1e-12, 1.0, O.ORDER_NONE)
     r = np.random.default_rng(p).uniform(-1, 1, A.nrows)
     assert_bitwise(pmg.ilut_apply(Fg, r), Fo.apply(r), "skew ilut_apply")
+
+
+def test_concurrent_solves_share_a_hierarchy():
+    """the hierarchy is immutable and shareable, each solve owns its vectors.
+    Two host threads solve on one hierarchy through two work objects at once (their sweeps run
+    concurrently on two streams); both must equal the oracle bit for bit."""
+    import ctypes
+    import threading
+    pb = P.build(P.make_spec(geometry="annulus", rhs="annulus", degrees=(3, 1), h_exp=6))
+    Hg = pmg.build_hierarchy(pb, smoother="ilut")
+    uo, ro = O.Hierarchy(pb, smoother=O.ILUT).solve(pb.f, pb.u0)
+    L = pmg.lib()
+    w2 = ctypes.c_void_p()
+    assert L.pmg_work_create(Hg.h, ctypes.byref(w2)) == 0
+    results = {}
+
+    def run(tag, work):
+        u = np.array(pb.u0, dtype=np.float64, copy=True)
+        hist = np.zeros(201)
+        cyc, flags, secs = ctypes.c_int(), ctypes.c_int(), ctypes.c_double()
+        for _ in range(3):
+            u[:] = pb.u0
+            st = L.pmg_solve(work, pmg.ptr(np.ascontiguousarray(pb.f)), pmg.ptr(u), 1e-8, 200, pmg.ptr(hist),
+                             ctypes.byref(cyc), ctypes.byref(flags), ctypes.byref(secs))
+            assert st == 0
+        results[tag] = (u.copy(), cyc.value)
+
+    try:
+        ts = [threading.Thread(target=run, args=("a", Hg.w)), threading.Thread(target=run, args=("b", w2.value))]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+    finally:
+        L.pmg_work_destroy(w2.value)
+    for tag in ("a", "b"):
+        u, c = results[tag]
+        assert c == ro["cycles"]
+        assert_bitwise(u, uo, f"concurrent solve {tag}")
