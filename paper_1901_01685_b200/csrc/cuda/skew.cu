@@ -34,8 +34,8 @@ namespace pmg {
 
 namespace {
 
-constexpr int G = 16;         // steps per bulk copy
-constexpr int NG = 4;         // bulk-copy groups in the ring
+constexpr int G = 32;         // steps per bulk copy
+constexpr int NG = 2;         // bulk-copy groups in the ring
 constexpr int PF = G * NG;    // steps staged
 constexpr int ICH = 3;        // 16-B chunks per (step, lane) item
 constexpr int STEP_BYTES = ICH * 32 * 16;
