@@ -64,6 +64,20 @@ int iga_problem_vec_copy(const iga_problem* h, int kind, int l, double* out);
 int iga_matrix_build(int kind, int geometry, int p, int p2, int nel, const double* D, const double* v, double R,
                      double nitsche_scale, iga_problem** out);
 
+/* MatrixMarket I/O.  Reading accepts coordinate real / integer / pattern
+ * matrices, general / symmetric / skew-symmetric (mirrored), and returns sorted CSR with duplicates
+ * summed in file order: call iga_mm_read_shape, allocate, then iga_mm_read.  Writing emits
+ * "coordinate real general" with %.17g values (exact round trip); comment may be NULL.  Vectors:
+ * one-column "array" files or plain text, one value per line.  Return 0 / -1 (iga_mm_last_error). */
+const char* iga_mm_last_error(void);
+int iga_mm_read_shape(const char* path, int32_t* nrows, int32_t* ncols, int64_t* nnz);
+int iga_mm_read(const char* path, int32_t* rowptr, int32_t* col, double* val);
+int iga_mm_write(const char* path, int32_t nrows, int32_t ncols, const int32_t* rowptr, const int32_t* col,
+                 const double* val, const char* comment);
+int iga_mm_write_vector(const char* path, int32_t n, const double* v);
+int iga_mm_read_vector_len(const char* path, int32_t* n);
+int iga_mm_read_vector(const char* path, double* v);
+
 /* SPEC.md:61-78 and :79-87 (used by the property tests) */
 int iga_eval_basis(int p, int spans, double x, int with_deriv, double* N, double* dN);
 int iga_geometry_map(int geometry, int patch, double xi, double eta, double* X, double* J);
