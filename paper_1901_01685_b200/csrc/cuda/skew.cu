@@ -308,12 +308,15 @@ __global__ void __launch_bounds__(NT) k_skew(SkewArgs a) {
         };
         double res = 0.0, xprev = 0.0;
         int hr = INT_MIN / 2;  // last seen halo_ready
-        Pre f;
+        Pre fa, fb;  // double-buffered step data: even steps of a group read fa, odd steps fb
         group_wait(0);
-        fetch(0, f);
+        fetch(0, fa);
+        static_assert(G % 2 == 0, "double-buffered step data needs an even group length");
         for (int tb = 0; tb < NS; tb += G) {
 #pragma unroll
             for (int u = 0; u < G; ++u) {
+                Pre& f = (u & 1) ? fb : fa;
+                Pre& fnext = (u & 1) ? fa : fb;
                 const int t = tb + u;
                 const int ix = t - P - D * k;  // the segment's stage-0 row at this step
                 if (u == G - 1) group_wait(unsigned(tb) / G + 1);  // for fetch(t + 1) below
@@ -356,7 +359,7 @@ __global__ void __launch_bounds__(NT) k_skew(SkewArgs a) {
                 }
                 xprev = x;
                 if (g0 > 0) hr = ld_vol_s(&sm.halo_ready);  // for the next step's test
-                fetch(t + 1, f);  // static data of the next step
+                fetch(t + 1, fnext);  // static data of the next step
             }
             // group tb/G fully consumed: hand its rhs slots back, refill its item slots
             __syncwarp();
