@@ -672,9 +672,8 @@ bool skew_plan(const Sell& S, const double* dinv, int32_t seg, SkewKind kind, in
     PMG_CUDA(cudaStreamSynchronize(st));
     if (h[0]) {
         if (getenv("PMG_VERBOSE"))
-            fprintf(stderr, "[pmg] skew plan rejected (n=%d seg=%d NR=%d): %s%s%s%s\n", S.n, seg, NR,
-                    h[0] & 1 ? "unsorted " : "", h[0] & 2 ? "row too long " : "", h[0] & 4 ? "own value late " : "",
-                    h[0] & 8 ? "term > 8 segments back" : "");
+            fprintf(stderr, "[pmg] skew plan rejected (n=%d seg=%d NR=%d): %s%s%s\n", S.n, seg, NR,
+                    h[0] & 1 ? "unsorted " : "", h[0] & 2 ? "row too long " : "", h[0] & 4 ? "own value late" : "");
         return fail();
     }
     const int dm = std::max(h[2], 1);
@@ -690,7 +689,12 @@ bool skew_plan(const Sell& S, const double* dinv, int32_t seg, SkewKind kind, in
     }
     int ry = 64;
     while (ry <= need) ry *= 2;
-    if (ry > 1024 || smem_bytes(NR, dm, ry, max_far) > 227 * 1024) return fail();
+    if (ry > 1024 || smem_bytes(NR, dm, ry, max_far) > 227 * 1024) {
+        if (getenv("PMG_VERBOSE"))
+            fprintf(stderr, "[pmg] skew plan rejected (n=%d seg=%d NR=%d): rings of %d rows or %d far values exceed "
+                            "shared memory\n", S.n, seg, NR, ry, max_far);
+        return fail();
+    }
     int32_t *far_off = nullptr, *far_idx = nullptr, *far_blk = nullptr;
     int* done = nullptr;
     PMG_CUDA(cudaMalloc(&far_off, sizeof(int32_t) * (nblk + 1)));
