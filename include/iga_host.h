@@ -19,9 +19,12 @@ extern "C" {
 #endif
 
 enum { IGA_GEOM_SQUARE = 0, IGA_GEOM_ANNULUS = 1, IGA_GEOM_LSHAPE = 2 };
-enum { IGA_RHS_SINSIN = 0, IGA_RHS_ANNULUS = 1, IGA_RHS_ONE = 2, IGA_RHS_B1 = 3, IGA_RHS_B2 = 4 };
+enum { IGA_RHS_SINSIN = 0, IGA_RHS_ANNULUS = 1, IGA_RHS_ONE = 2, IGA_RHS_B1 = 3, IGA_RHS_B2 = 4, IGA_RHS_B3 = 5 };
 enum { IGA_MAT_A = 0, IGA_MAT_P = 1, IGA_MAT_PT = 2, IGA_MAT_HA = 3, IGA_MAT_HP = 4, IGA_MAT_HPT = 5 };
 enum { IGA_VEC_ML = 0, IGA_VEC_F = 1, IGA_VEC_U0 = 2 };
+/* multipatch DOF numbering: patch-major (glued DOFs keep the lower patch's index) or global
+ * row-major over the domain's control grid (y, then x ascending) */
+enum { IGA_NUMBER_PATCH = 0, IGA_NUMBER_ROWMAJOR = 1 };
 
 typedef struct iga_problem_spec {
     int geometry;        /* IGA_GEOM_* */
@@ -36,6 +39,7 @@ typedef struct iga_problem_spec {
     int random_guess;    /* 0: u0 = 0; 1: splitmix64(seed) mapped to U[-1,1) */
     uint64_t seed;
     double nitsche_scale; /* multiplies the Nitsche penalty eta = 4 k^2 (0 -> 1) */
+    int numbering;        /* IGA_NUMBER_* (multipatch only) */
 } iga_problem_spec;
 
 typedef struct iga_problem_s iga_problem;

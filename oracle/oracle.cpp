@@ -6,6 +6,7 @@
 #include "oracle.h"
 
 #include <algorithm>
+#include <functional>
 #include <climits>
 #include <chrono>
 #include <cmath>
@@ -396,6 +397,100 @@ static std::unique_ptr<Factor> ilut(const pmg_csr_view& A, double tau, double m,
     return F;
 }
 
+// PROBE ONLY: the dual-threshold ILUT of the paper's library (PAPER.md:311,
+// Eigen's IncompleteLUT), restated from its published algorithm to explain the gap
+// between the SPEC's rule and the paper's tables.  Differences from ilut() above:
+//   * fill_in = floor(m nnz / n) + 1, and only nnzL = fill_in / 2 entries are kept in L; U keeps
+//     min(|U row incl. diagonal|, nnzL) - 1 off-diagonal entries;
+//   * a multiplier is dropped when |w_k / u_kk| <= tau (absolute), U entries when
+//     |w_j| <= tau * ||row||_2 (2-norm of the original row);
+//   * a zero pivot is shifted to sqrt(tau) * ||row||_2 instead of being an error.
+// The fill-reducing ordering (the library's AMD) is not restated; `perm` is natural or RCM.
+static std::unique_ptr<Factor> ilut_eigen(const pmg_csr_view& A, double tau, double m, int ordering) {
+    const int32_t n = A.nrows;
+    auto F = std::make_unique<Factor>();
+    F->n = n;
+    F->perm = ordering == PMG_ORDER_RCM ? rcm(A) : std::vector<int32_t>(n);
+    if (ordering != PMG_ORDER_RCM)
+        for (int32_t i = 0; i < n; ++i) F->perm[i] = i;
+    F->pinv.assign(n, 0);
+    for (int32_t i = 0; i < n; ++i) F->pinv[F->perm[i]] = i;
+    const int64_t nnz = A.rowptr[n];
+    int64_t fill_in = int64_t(double(nnz) * m) / n + 1;
+    if (fill_in > n) fill_in = n;
+    const int64_t nnzL = fill_in / 2, nnzU = nnzL;
+    std::vector<RowOut> Lr(n), Ur(n);
+    std::vector<double> w(n, 0.0);
+    std::vector<char> present(n, 0);
+    std::vector<int32_t> touched;
+    for (int32_t i = 0; i < n; ++i) {
+        const int32_t old = F->perm[i];
+        double rn = 0.0;
+        touched.clear();
+        std::vector<int32_t> lpos;
+        for (int32_t k = A.rowptr[old]; k < A.rowptr[old + 1]; ++k) {
+            int32_t c = F->pinv[A.col[k]];
+            w[c] = A.val[k];
+            present[c] = 1;
+            touched.push_back(c);
+            if (c < i) lpos.push_back(c);
+            rn = rn + A.val[k] * A.val[k];
+        }
+        rn = std::sqrt(rn);
+        std::vector<Cand> lc, uc;
+        // pivots in ascending column order, including fill (a min-heap over the L part)
+        std::vector<int32_t> heap(lpos.begin(), lpos.end());
+        std::make_heap(heap.begin(), heap.end(), std::greater<int32_t>());
+        while (!heap.empty()) {
+            std::pop_heap(heap.begin(), heap.end(), std::greater<int32_t>());
+            const int32_t k = heap.back();
+            heap.pop_back();
+            const RowOut& Uk = Ur[k];
+            const double fact = w[k] / Uk.v[0];
+            if (std::fabs(fact) <= tau) continue;
+            for (size_t q = 1; q < Uk.c.size(); ++q) {
+                const int32_t j = Uk.c[q];
+                if (!present[j]) {
+                    present[j] = 1;
+                    w[j] = 0.0;
+                    touched.push_back(j);
+                    if (j < i) {
+                        heap.push_back(j);
+                        std::push_heap(heap.begin(), heap.end(), std::greater<int32_t>());
+                    }
+                }
+                w[j] = w[j] - fact * Uk.v[q];
+            }
+            lc.push_back({k, fact});
+        }
+        double diag = present[i] ? w[i] : 0.0;
+        if (diag == 0.0) diag = std::sqrt(tau) * rn;
+        for (int32_t c : touched)
+            if (c > i && std::fabs(w[c]) > tau * rn) uc.push_back({c, w[c]});
+        keep_largest(lc, int32_t(std::min<int64_t>(int64_t(lc.size()), nnzL)));
+        const int64_t keepU = std::min<int64_t>(int64_t(uc.size()) + 1, nnzU) - 1;
+        keep_largest(uc, int32_t(std::max<int64_t>(keepU, 0)));
+        for (auto& e : lc) { Lr[i].c.push_back(e.c); Lr[i].v.push_back(e.v); }
+        Ur[i].c.push_back(i);
+        Ur[i].v.push_back(diag);
+        for (auto& e : uc) { Ur[i].c.push_back(e.c); Ur[i].v.push_back(e.v); }
+        for (int32_t c : touched) { w[c] = 0.0; present[c] = 0; }
+    }
+    F->L.n = F->L.m = F->U.n = F->U.m = n;
+    F->L.rp.assign(n + 1, 0);
+    F->U.rp.assign(n + 1, 0);
+    for (int32_t i = 0; i < n; ++i) {
+        F->L.rp[i + 1] = F->L.rp[i] + int32_t(Lr[i].c.size());
+        F->U.rp[i + 1] = F->U.rp[i] + int32_t(Ur[i].c.size());
+        F->L.ci.insert(F->L.ci.end(), Lr[i].c.begin(), Lr[i].c.end());
+        F->L.v.insert(F->L.v.end(), Lr[i].v.begin(), Lr[i].v.end());
+        F->U.ci.insert(F->U.ci.end(), Ur[i].c.begin(), Ur[i].c.end());
+        F->U.v.insert(F->U.v.end(), Ur[i].v.begin(), Ur[i].v.end());
+    }
+    F->levels();
+    return F;
+}
+
 // e = P^T U^{-1} L^{-1} P r.  L rows ascending, U rows descending.
 static void lsolve(const Factor& F, const double* r, double* y) {
     for (int32_t i = 0; i < F.n; ++i) {
@@ -690,6 +785,11 @@ int orc_ilut(const pmg_csr_view* A, double tau, double fillfactor, int ordering,
     auto F = ilut(*A, tau, fillfactor, ordering, err_row);
     if (!F) return PMG_ZERO_PIVOT;
     *out = new orc_factor_s{F.release(), true};
+    return PMG_OK;
+}
+int orc_ilut_eigen(const pmg_csr_view* A, double tau, double fillfactor, int ordering, orc_factor* out) {
+    if (A->nrows != A->ncols) return PMG_ERR_DIM;
+    *out = new orc_factor_s{ilut_eigen(*A, tau, fillfactor, ordering).release(), true};
     return PMG_OK;
 }
 int orc_factor_from_arrays(int32_t n, const int32_t* Lrp, const int32_t* Lc, const double* Lv, const int32_t* Urp,

@@ -43,6 +43,8 @@ double orc_norm2(const double* r, int64_t n); /* canonical blocked order (DESIGN
 int orc_gs_sweep(const pmg_csr_view* A, double* u, const double* f, int64_t* err_row);
 int orc_rcm(const pmg_csr_view* A, int32_t* perm);
 int orc_ilut(const pmg_csr_view* A, double tau, double fillfactor, int ordering, orc_factor* out, int64_t* err_row);
+/* PROBE ONLY: the paper library's ILUT rule (half cap per triangle, 2-norm threshold) */
+int orc_ilut_eigen(const pmg_csr_view* A, double tau, double fillfactor, int ordering, orc_factor* out);
 int orc_factor_from_arrays(int32_t n, const int32_t* L_rowptr, const int32_t* L_col, const double* L_val,
                            const int32_t* U_rowptr, const int32_t* U_col, const double* U_val, const int32_t* perm,
                            orc_factor* out);

@@ -52,6 +52,7 @@ def lib():
         L.orc_gs_sweep.argtypes = [vp, vp, vp, vp]
         L.orc_rcm.argtypes = [vp, vp]
         L.orc_ilut.argtypes = [vp, dbl, dbl, ctypes.c_int, ctypes.POINTER(vp), vp]
+        L.orc_ilut_eigen.argtypes = [vp, dbl, dbl, ctypes.c_int, ctypes.POINTER(vp)]
         L.orc_factor_from_arrays.argtypes = [i32, vp, vp, vp, vp, vp, vp, vp, ctypes.POINTER(vp)]
         L.orc_factor_free.argtypes = [vp]
         L.orc_factor_stats.argtypes = [vp, vp, vp, vp, vp]
@@ -200,6 +201,15 @@ def ilut_factorize(A, tau=1e-12, fillfactor=1.0, ordering=ORDER_RCM) -> Factor:
     st = lib().orc_ilut(ctypes.byref(view(A)), tau, fillfactor, ordering, ctypes.byref(h), ctypes.byref(row))
     if st != PMG_OK:
         raise OracleError(st, row.value)
+    f = Factor(h.value)
+    f.n = A.nrows
+    return f
+
+
+def ilut_factorize_eigen(A, tau=1e-12, fillfactor=1.0, ordering=ORDER_NONE) -> Factor:
+    """PROBE ONLY: the paper library's ILUT rule (oracle.cpp ilut_eigen)."""
+    h = ctypes.c_void_p()
+    lib().orc_ilut_eigen(ctypes.byref(view(A)), tau, fillfactor, ordering, ctypes.byref(h))
     f = Factor(h.value)
     f.n = A.nrows
     return f

@@ -208,6 +208,28 @@ Space Space::build(const Domain& dom, int p, int nel) {
             if (sp.l2g[P][i] < 0) sp.l2g[P][i] = next++;
     }
     sp.ndof = next;
+    if (dom.rowmajor && np > 1) {
+        // global row-major renumbering: key (gy, gx) of the DOF in the domain's control grid
+        std::vector<int64_t> key(next, -1);
+        const int64_t W = int64_t(n) * 8;
+        for (int P = 0; P < np; ++P)
+            for (int iy = 0; iy < n; ++iy)
+                for (int ix = 0; ix < n; ++ix) {
+                    const int64_t gx = ix + int64_t(dom.grid_off[P][0]) * (n - 1);
+                    const int64_t gy = iy + int64_t(dom.grid_off[P][1]) * (n - 1);
+                    const int64_t k = gy * W + gx;
+                    int64_t& slot = key[sp.l2g[P][ix + iy * n]];
+                    if (slot >= 0 && slot != k) throw AssemblyError("row-major numbering: glue is not conforming");
+                    slot = k;
+                }
+        std::vector<int32_t> order(next);
+        for (int32_t i = 0; i < next; ++i) order[i] = i;
+        std::sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return key[a] < key[b]; });
+        std::vector<int32_t> rank(next);
+        for (int32_t r = 0; r < next; ++r) rank[order[r]] = r;
+        for (auto& m : sp.l2g)
+            for (auto& g : m) g = rank[g];
+    }
     return sp;
 }
 
@@ -362,7 +384,9 @@ static void scatter(HostCsr& A, const std::vector<int32_t>& rmap, const std::vec
 // ------------------------------------------------------------------ assembly
 // a(u,v) = int (D grad u).grad v + (v.grad u) v + R u v  +  symmetric Nitsche on the
 // Dirichlet boundary:  - int (D grad u.n) v - int (D grad v.n) u + (eta/h) int u v,
-// eta = 4 p^2, h = 1/nel.  rhs = (f, v) (g = 0).
+// eta = 4 p^2, h = 1/nel.  rhs = (f, v), plus the Nitsche
+// consistency terms -int (D grad v.n) g + (eta/h) int g v of inhomogeneous Dirichlet data g
+// (Benchmark 3).
 HostCsr assemble_operator(const Domain& dom, const Space& sp, const Cdr& c, std::vector<double>* rhs) {
     HostCsr A = make_pattern(dom, sp, sp);
     const int p = sp.p, nel = sp.nel, n1 = p + 1, n = nel + p, nq = p + 1;
@@ -376,7 +400,7 @@ HostCsr assemble_operator(const Domain& dom, const Space& sp, const Cdr& c, std:
         const auto& l2g = sp.l2g[P];
         for_each_element_strip(nel, p + 1, [&](int ey) {
             std::vector<double> E(size_t(nloc2) * nloc2), S(4 * size_t(nq) * n1 * n1);
-            std::vector<double> K(4 * nq * nq), C(2 * nq * nq), Mr(nq * nq), Fq(nq * nq);
+            std::vector<double> K(4 * nq * nq), C(2 * nq * nq), Mr(nq * nq), Fq(nq * nq), Fb(nloc2);
             for (int ex = 0; ex < nel; ++ex) {
                 // geometric factors at the (p+1)^2 points
                 for (int b = 0; b < nq; ++b)
@@ -439,6 +463,7 @@ HostCsr assemble_operator(const Domain& dom, const Space& sp, const Cdr& c, std:
                         }
                 }
                 // Nitsche terms on Dirichlet edges touched by this element
+                std::fill(Fb.begin(), Fb.end(), 0.0);
                 for (int edge = 0; edge < 4; ++edge) {
                     bool on = (edge == 0 && ey == 0) || (edge == 1 && ex == nel - 1) || (edge == 2 && ey == nel - 1) ||
                               (edge == 3 && ex == 0);
@@ -474,6 +499,10 @@ HostCsr assemble_operator(const Domain& dom, const Space& sp, const Cdr& c, std:
                         for (int te = 0; te < nloc2; ++te)
                             for (int tr = 0; tr < nloc2; ++tr)
                                 E[size_t(te) * nloc2 + tr] += w * (-flux[tr] * phi[te] - flux[te] * phi[tr] + pen * phi[te] * phi[tr]);
+                        if (rhs && c.g) {  // consistency terms of inhomogeneous data: -int (D grad v.n) g + (eta/h) int g v
+                            const double gv = c.g(X[0], X[1]);
+                            for (int te = 0; te < nloc2; ++te) Fb[te] += w * (-flux[te] * gv + pen * phi[te] * gv);
+                        }
                     }
                 }
                 scatter(A, l2g, l2g, n, n, ex, ey, n1, n1, E.data());
@@ -483,7 +512,7 @@ HostCsr assemble_operator(const Domain& dom, const Space& sp, const Cdr& c, std:
                             double acc = 0;
                             for (int b = 0; b < nq; ++b)
                                 for (int a = 0; a < nq; ++a) acc += Fq[a + b * nq] * bs.b(ex, a)[i1] * bs.b(ey, b)[j1];
-                            (*rhs)[l2g[(ex + i1) + (ey + j1) * n]] += acc;
+                            (*rhs)[l2g[(ex + i1) + (ey + j1) * n]] += acc + Fb[i1 + j1 * n1];
                         }
                 }
             }

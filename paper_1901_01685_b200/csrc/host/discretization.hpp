@@ -12,6 +12,7 @@
 //                  DOF identification; patch-major numbering)
 #pragma once
 
+#include <array>
 #include <cstdint>
 #include <functional>
 #include <stdexcept>
@@ -62,6 +63,7 @@ struct Cdr {
     double R = 0;
     double nitsche_scale = 1.0;
     std::function<double(double, double)> f;
+    std::function<double(double, double)> g;  // Dirichlet data (null: homogeneous)
 };
 
 // edge ids: 0 eta=0 (iy=0), 1 xi=1 (ix=n-1), 2 eta=1 (iy=n-1), 3 xi=0 (ix=0)
@@ -70,6 +72,11 @@ struct Interface { int pa, ea, pb, eb; };  // edge ea of patch pa == edge eb of 
 struct Domain {
     std::vector<NurbsPatch> patches;
     std::vector<Interface> glue;     // conforming interfaces (pb < pa: pa's DOFs take pb's index)
+    // Optional global DOF numbering for multipatch domains whose patches tile a grid of unit
+    // squares: patch P sits at grid cell grid_off[P] = {cx, cy}; DOFs are then numbered
+    // row-major over the whole domain (y, then x ascending) instead of patch-major.
+    std::vector<std::array<int, 2>> grid_off;
+    bool rowmajor = false;
     bool is_interface(int patch, int edge) const;
 };
 

@@ -38,7 +38,7 @@ static uint64_t splitmix64(uint64_t& s) {
     return z ^ (z >> 31);
 }
 
-static Domain make_domain(int geometry) {
+static Domain make_domain(int geometry, int numbering) {
     Domain d;
     if (geometry == IGA_GEOM_SQUARE) d.patches.push_back(NurbsPatch::affine(0, 0, 1, 1));
     else if (geometry == IGA_GEOM_ANNULUS) d.patches.push_back(NurbsPatch::quarter_annulus(1.0, 2.0));
@@ -49,6 +49,8 @@ static Domain make_domain(int geometry) {
         d.patches.push_back(NurbsPatch::affine(0, -1, 1, 1));
         d.glue.push_back({1, 2, 0, 0});  // patch1 top  == patch0 bottom
         d.glue.push_back({2, 3, 1, 1});  // patch2 left == patch1 right
+        d.grid_off = {{0, 1}, {0, 0}, {1, 0}};
+        d.rowmajor = numbering == IGA_NUMBER_ROWMAJOR;
     } else
         throw ConfigError("unknown geometry");
     return d;
@@ -90,6 +92,17 @@ static Cdr make_coeffs(int rhs_kind, const double* D, const double* v, double R)
             };
             break;
         }
+        case IGA_RHS_B3: {  // paper Benchmark 3: harmonic corner singularity,
+                            // f = 0, inhomogeneous Dirichlet data g = u through Nitsche
+            c.f = [](double, double) { return 0.0; };
+            c.g = [](double x, double y) {
+                const double r23 = std::cbrt(x * x + y * y);
+                const double th = std::atan2(y, x);
+                // y = 0, x > 0 is the re-entrant edge: the y < 0 branch (u = 0 there)
+                return (y > 0 || (y == 0 && x < 0)) ? r23 * std::sin((2.0 * th - M_PI) / 3.0) : r23 * std::sin((2.0 * th + 3.0 * M_PI) / 3.0);
+            };
+            break;
+        }
         default:
             throw ConfigError("unknown rhs kind");
     }
@@ -103,7 +116,7 @@ static Problem build_problem(const iga_problem_spec& s) {
         if (!(s.degrees[i] < s.degrees[i - 1])) throw ConfigError("degrees must be strictly decreasing");
     if (s.h_exp < 2 || s.h_exp > 12) throw ConfigError("h_exp out of range");
     if (s.coarsest_h_exp < 1 || s.coarsest_h_exp > s.h_exp) throw ConfigError("coarsest_h_exp out of range");
-    Domain dom = make_domain(s.geometry);
+    Domain dom = make_domain(s.geometry, s.numbering);
     Cdr c = make_coeffs(s.rhs, s.D, s.v, s.R);
     c.nitsche_scale = s.nitsche_scale > 0 ? s.nitsche_scale : 1.0;
     Cdr c_nof = c;
@@ -281,7 +294,7 @@ int iga_problem_vec_copy(const iga_problem* h, int kind, int l, double* out) {
 int iga_matrix_build(int kind, int geometry, int p, int p2, int nel, const double* D, const double* v, double R,
                      double nitsche_scale, iga_problem** out) {
     try {
-        Domain dom = make_domain(geometry);
+        Domain dom = make_domain(geometry, IGA_NUMBER_PATCH);
         Space sp = Space::build(dom, p, nel);
         auto* h = new iga_problem_s;
         h->pb.plev.resize(1);
@@ -328,7 +341,7 @@ int iga_eval_basis(int p, int spans, double x, int with_deriv, double* N, double
 
 int iga_geometry_map(int geometry, int patch, double xi, double eta, double* X, double* J) {
     try {
-        Domain d = make_domain(geometry);
+        Domain d = make_domain(geometry, IGA_NUMBER_PATCH);
         double Jm[2][2];
         d.patches.at(patch).map(xi, eta, X, Jm);
         J[0] = Jm[0][0]; J[1] = Jm[0][1]; J[2] = Jm[1][0]; J[3] = Jm[1][1];

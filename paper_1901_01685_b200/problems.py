@@ -14,7 +14,7 @@ import numpy as np
 from ._native import Csr, load, ptr
 
 GEOM = {"square": 0, "annulus": 1, "lshape": 2}
-RHS = {"sinsin": 0, "annulus": 1, "one": 2, "b1": 3, "b2": 4}
+RHS = {"sinsin": 0, "annulus": 1, "one": 2, "b1": 3, "b2": 4, "b3": 5}
 MAT_A, MAT_P, MAT_PT, MAT_HA, MAT_HP, MAT_HPT = range(6)
 VEC_ML, VEC_F, VEC_U0 = range(3)
 
@@ -25,6 +25,7 @@ class ProblemSpec(ctypes.Structure):
         ("v", ctypes.c_double * 2), ("R", ctypes.c_double), ("h_exp", ctypes.c_int),
         ("coarsest_h_exp", ctypes.c_int), ("n_degrees", ctypes.c_int), ("degrees", ctypes.c_int * 8),
         ("random_guess", ctypes.c_int), ("seed", ctypes.c_uint64), ("nitsche_scale", ctypes.c_double),
+        ("numbering", ctypes.c_int),
     ]
 
 
@@ -99,8 +100,11 @@ def config_spec(config: int, degree: int = 0) -> ProblemSpec:
     return s
 
 
+NUMBERING = {"patch": 0, "rowmajor": 1}
+
+
 def make_spec(geometry="square", rhs="one", degrees=(2, 1), h_exp=4, D=(1, 0, 0, 1), v=(0, 0), R=0.0,
-              random_guess=False, seed=42, coarsest_h_exp=2) -> ProblemSpec:
+              random_guess=False, seed=42, coarsest_h_exp=2, numbering="patch") -> ProblemSpec:
     s = ProblemSpec()
     s.geometry = GEOM[geometry]
     s.rhs = RHS[rhs]
@@ -115,17 +119,22 @@ def make_spec(geometry="square", rhs="one", degrees=(2, 1), h_exp=4, D=(1, 0, 0,
         s.degrees[i] = d
     s.random_guess = int(bool(random_guess))
     s.seed = seed
+    s.numbering = NUMBERING[numbering]
     return s
 
 
 def benchmark_spec(bench: int, p: int, h_exp: int, consecutive=True, seed=42) -> ProblemSpec:
-    """Paper Benchmarks 1/2 with the paper's random initial guess."""
+    """Paper Benchmarks 1-3 with the paper's random initial guess.
+    Benchmark 3 is the L-shape as 3 conforming patches with inhomogeneous Dirichlet
+    data g = u_exact imposed through Nitsche and f = 0 (u_exact is harmonic)."""
     degrees = tuple(range(p, 0, -1)) if consecutive else (p, 1)
     if bench == 1:
         return make_spec("annulus", "b1", degrees, h_exp, random_guess=True, seed=seed)
     if bench == 2:
         return make_spec("square", "b2", degrees, h_exp, D=(1.2, -0.7, -0.4, 0.9), v=(0.4, -0.2), R=0.3,
                          random_guess=True, seed=seed)
+    if bench == 3:
+        return make_spec("lshape", "b3", degrees, h_exp, random_guess=True, seed=seed)
     raise ValueError(bench)
 
 
