@@ -146,3 +146,21 @@ def test_spec6_annulus_gauss_seidel_documented_gap():
     (0.368, 0.707, 0.916) -- the documented annulus GS gap."""
     got = [_rho("annulus", p, 4, O.GS) for p in (2, 3, 4)]
     assert np.allclose(got, (0.368, 0.707, 0.916), atol=0.002)
+
+
+# ---------------------------------------------------------------- Table 1 (SPEC.md:139)
+def _kappa(geometry, h_exp, level):
+    import scipy.sparse as sp
+    pb = P.build(P.make_spec(geometry, "one", (2, 1), h_exp))
+    A = pb.plevels[level].A
+    return float(np.linalg.cond(sp.csr_matrix((A.val, A.col, A.rowptr), shape=(A.nrows, A.ncols)).toarray()))
+
+
+def test_table1_condition_numbers_documented_gap():
+    """SPEC.md:139 / PAPER.md Table 1: kappa(A_{h,1}) on the annulus is 9.78e2 at h = 2^-4.  The
+    exact-NURBS annulus of SPEC.md:86/:97 gives 104 (the unit square 51.8), growing as h^-2 like the
+    paper's; the paper's annulus operator is ~9x worse conditioned."""
+    k4, k5 = _kappa("annulus", 4, 1), _kappa("annulus", 5, 1)
+    assert abs(k4 - 104) < 1 and abs(k5 - 441) < 2
+    assert 3.9 < k5 / k4 < 4.5  # paper: 4.19e3 / 9.78e2 = 4.28
+    assert abs(_kappa("square", 4, 1) - 51.8) < 0.5
