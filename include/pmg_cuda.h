@@ -74,7 +74,7 @@ int pmg_factor_stats(pmg_factor F, int64_t* nnz_L, int64_t* nnz_U, int32_t* leve
                      int32_t* max_row_L, int32_t* max_row_U);
 /* which sweep kernels apply_factor uses for F (no reference counterpart; reporting):
  * level-scheduled, chained segments (seg = grid-row length) or skewed warps (lane skew D) */
-enum { PMG_SWEEP_LEVELS = 0, PMG_SWEEP_CHAIN = 1, PMG_SWEEP_SKEW = 2 };
+enum { PMG_SWEEP_LEVELS = 0, PMG_SWEEP_CHAIN = 1, PMG_SWEEP_SKEW = 2, PMG_SWEEP_WAVE = 3 };
 int pmg_factor_sweep_info(pmg_factor F, int32_t* kind, int32_t* seg, int32_t* skew_D_L, int32_t* skew_D_U);
 /* copy factors to host CSR arrays (L strictly lower, unit diagonal implicit; U with
  * diagonal); pass NULL arrays to query sizes only.  perm may be NULL. */

@@ -637,8 +637,21 @@ static int64_t smooth(Hier& H, int l, double* u, const double* f, const double* 
 
 // V-cycle at p-level l.  `zero`: u == 0 on entry (its residual is f).
 static int64_t vcycle(Hier& H, int l, double* u, const double* f, const double* r_known, bool zero) {
-    if (l == H.np - 1) {  // p = 1: one h-MG V-cycle from zero
-        hmg(H, 0, u, f);
+    if (l == H.np - 1) {  // p = 1: one h-MG V-cycle on the residual equation
+        if (zero) {  // u == 0: the correction is the cycle's result itself
+            hmg(H, 0, u, f);
+            return -1;
+        }
+        // a hierarchy of p = 1 alone: e = hmg(f - A u), u += e
+        PLev& L = H.pl[l];
+        const int32_t n = L.A.n;
+        const double* r = r_known;
+        if (!r) {
+            residual(L.A, u, f, L.r.data());
+            r = L.r.data();
+        }
+        hmg(H, 0, L.y.data(), r);
+        for (int32_t i = 0; i < n; ++i) u[i] = u[i] + L.y[i];
         return -1;
     }
     PLev& L = H.pl[l];

@@ -20,6 +20,7 @@
 #include "skew.cuh"
 #include "sell.cuh"
 #include "trsv.cuh"
+#include "wave.cuh"
 
 using namespace pmg;
 
@@ -120,8 +121,10 @@ struct pmg_csr_s {
     int32_t* gs_split = nullptr;
     int32_t gs_gap = 0;
     bool gs_chain = false;        // chained GS sweep (else level-scheduled)
-    bool gs_skew = false;         // skewed-warp GS sweep (default for tensor-grid orderings)
+    bool gs_skew = false;         // skewed-warp GS sweep
     SkewPlan gs_plan;
+    bool gs_wave = false;         // rotating-lane GS sweep (default for tensor-grid orderings)
+    WavePlan gs_wplan;
     ~pmg_csr_s() {
         A.free();
         sell_free(S);
@@ -132,6 +135,7 @@ struct pmg_csr_s {
             cudaFree(gs_nlow);
             cudaFree(gs_split);
             skew_plan_free(gs_plan);
+            wave_plan_free(gs_wplan);
         }
     }
 };
@@ -150,6 +154,8 @@ struct pmg_factor_s {
     int32_t* rev = nullptr;           // v -> row for the U sweep (descending rows)
     int32_t *splitL = nullptr, *splitU = nullptr;
     bool skew = false;                // skewed-warp sweeps (short rows, short reach)
+    bool wave = false;                // rotating-lane sweeps (default for tensor-grid orderings)
+    WavePlan waveL, waveU;
     int32_t bs = 32;                  // chain finisher batch
     int32_t gapL = 0, gapU = 0;       // chain start gates
     SkewPlan planL, planU;
@@ -167,6 +173,8 @@ struct pmg_factor_s {
         cudaFree(splitU);
         skew_plan_free(planL);
         skew_plan_free(planU);
+        wave_plan_free(waveL);
+        wave_plan_free(waveU);
     }
 };
 
@@ -174,7 +182,12 @@ namespace {
 
 // e = U^{-1} L^{-1} r[perm] added into u[perm]  (y, x: scratch)
 void apply_factor(pmg_factor_s* F, const double* r, double* y, double* x, double* u, int* ticket, cudaStream_t st) {
-    if (F->skew) {
+    if (F->wave) {
+        WaveOp l{kSkewL, &F->waveL, r, y, nullptr};
+        wave_sweep(l, ticket, st);
+        WaveOp up{kSkewU, &F->waveU, y, x, u};
+        wave_sweep(up, ticket, st);
+    } else if (F->skew) {
         SkewOp l{kSkewL, &F->planL, r, y, nullptr};
         skew_sweep(l, ticket, st);
         SkewOp up{kSkewU, &F->planU, y, x, u};
@@ -193,7 +206,10 @@ void apply_factor(pmg_factor_s* F, const double* r, double* y, double* x, double
 // su: n doubles of caller scratch (the skew pre-pass writes the upper sums there)
 void gs_apply(pmg_csr_s* A, const double* f, const double* uo, double* un, double* su, int* ticket,
               cudaStream_t st) {
-    if (A->gs_skew) {
+    if (A->gs_wave) {
+        WaveOp g{kSkewGS, &A->gs_wplan, f, un, nullptr, &A->gs, A->gs_nlow, uo, su};
+        wave_sweep(g, ticket, st);
+    } else if (A->gs_skew) {
         SkewOp g{kSkewGS, &A->gs_plan, f, un, nullptr, &A->gs, A->gs_nlow, uo, su};
         skew_sweep(g, ticket, st);
     } else if (A->gs_chain) {
@@ -260,7 +276,9 @@ void ensure_gs(pmg_csr_s* h, cudaStream_t st) {
         PMG_CUDA(cudaStreamSynchronize(st));
         int32_t mx = 0;
         for (int32_t v : nl) mx = std::max(mx, v);
-        h->gs_skew = skew_plan(h->gs, h->gs_diag, h->seg, kSkewGS, mx, h->gs_plan, st, h->gs_nlow);
+        const char* wv = getenv("PMG_WAVE");
+        if (!(wv && wv[0] == '0')) h->gs_wave = wave_plan(h->gs, h->gs_diag, h->seg, kSkewGS, mx, h->gs_wplan, st, h->gs_nlow);
+        if (!h->gs_wave) h->gs_skew = skew_plan(h->gs, h->gs_diag, h->seg, kSkewGS, mx, h->gs_plan, st, h->gs_nlow);
     }
     h->gs_ready = true;
 }
@@ -349,7 +367,17 @@ int make_factor(pmg_csr_s* A, double tau, double fillfactor, int ordering, pmg_f
     // tensor-grid orderings: skewed-warp sweeps (skew.cu); PMG_SKEW=0 keeps the
     // chained-segment kernel for every factor
     const char* sk = getenv("PMG_SKEW");
-    if (F->seg > 0 && !F->perm && !(sk && sk[0] == '0')) {
+    const char* wv = getenv("PMG_WAVE");
+    if (F->seg > 0 && !F->perm && !(wv && wv[0] == '0')) {
+        const bool okL = wave_plan(F->Ls, nullptr, F->seg, kSkewL, F->max_row_L, F->waveL, st);
+        const bool okU = okL && wave_plan(F->Us, F->Udiag, F->seg, kSkewU, F->max_row_U - 1, F->waveU, st);
+        F->wave = okL && okU;
+        if (!F->wave) {
+            wave_plan_free(F->waveL);
+            wave_plan_free(F->waveU);
+        }
+    }
+    if (!F->wave && F->seg > 0 && !F->perm && !(sk && sk[0] == '0')) {
         const bool okL = skew_plan(F->Ls, nullptr, F->seg, kSkewL, F->max_row_L, F->planL, st);
         const bool okU = okL && skew_plan(F->Us, F->Udiag, F->seg, kSkewU, F->max_row_U - 1, F->planU, st);
         F->skew = okL && okU;
@@ -452,6 +480,15 @@ struct pmg_work_s {
     double cls_ms[kNumCls] = {};
     int64_t launches = 0;
     int64_t cls_launches[kNumCls] = {};
+    // one solve cycle (V-cycle + stop-test residual) captured as a CUDA graph:
+    // replayed per cycle, re-captured when the right-hand side buffer changes
+    cudaGraphExec_t gx = nullptr;
+    const double* gx_f = nullptr;
+    int gx_cur = -1;
+    int64_t gx_launches = 0;
+    int64_t gx_cls[kNumCls] = {};
+    double* rho_dev = nullptr;    // the cycle's rho (device), copied to rho_host by the graph
+    double* rho_host = nullptr;   // pinned
 
     ~pmg_work_s() {
         for (auto& p : pw) {
@@ -482,6 +519,9 @@ struct pmg_work_s {
             cudaEventDestroy(e.first);
             cudaEventDestroy(e.second);
         }
+        if (gx) cudaGraphExecDestroy(gx);
+        cudaFree(rho_dev);
+        cudaFreeHost(rho_host);
         if (st) cudaStreamDestroy(st);
     }
 
@@ -529,7 +569,16 @@ void smooth_ilut(pmg_work_s& W, pmg_csr_s* A, pmg_factor_s* F, double* u, const 
         rr = r;
     }
     // launch counts: our kernels per sweep (sentinel fill, sweep, and the U update pass)
-    if (F->skew) {
+    if (F->wave) {
+        W.run(fine ? kClsL0 : kClsCoarse, 2, [&] {
+            WaveOp l{kSkewL, &F->waveL, rr, y, nullptr};
+            wave_sweep(l, W.ticket, W.st);
+        });
+        W.run(fine ? kClsU0 : kClsCoarse, 3, [&] {
+            WaveOp up{kSkewU, &F->waveU, y, x, u};
+            wave_sweep(up, W.ticket, W.st);
+        });
+    } else if (F->skew) {
         W.run(fine ? kClsL0 : kClsCoarse, 2, [&] {
             SkewOp l{kSkewL, &F->planL, rr, y, nullptr};
             skew_sweep(l, W.ticket, W.st);
@@ -582,7 +631,7 @@ int smooth(pmg_work_s& W, int l, const double* f, const double* r_known) {
         if (L.A->gs_zero_row >= 0) return PMG_ZERO_DIAG;
         double* uo = w.u[w.cur];
         double* un = w.u[1 - w.cur];
-        W.run(fine ? kClsGS0 : kClsCoarse, L.A->gs_skew ? 3 : 2,
+        W.run(fine ? kClsGS0 : kClsCoarse, (L.A->gs_skew || L.A->gs_wave) ? 3 : 2,
               [&] { gs_apply(L.A, f, uo, un, w.y, W.ticket, W.st); });  // w.y: idle in GS mode
         w.cur = 1 - w.cur;
         return PMG_OK;
@@ -596,7 +645,21 @@ int vcycle(pmg_work_s& W, int l, const double* f, const double* r_known, bool ze
     pmg_hier_s& H = *W.H;
     PWork& w = W.pw[l];
     if (l == int(H.pl.size()) - 1) {
-        hmg(W, 0, w.u[w.cur], f);
+        if (zero) {  // u == 0: the h-MG correction is the new iterate
+            hmg(W, 0, w.u[w.cur], f);
+            return PMG_OK;
+        }
+        // a hierarchy of p = 1 alone: e = hmg(f - A u), u += e
+        PLev& L = H.pl[l];
+        const int32_t n = L.A->A.n;
+        const int cls = l == 0 ? kClsResid0 : kClsCoarse;
+        const double* r = r_known;
+        if (!r) {
+            W.run(cls, 1, [&] { sell_rowop(L.A->S, kOpResidual, w.u[w.cur], f, nullptr, w.r, nullptr, W.st); });
+            r = w.r;
+        }
+        hmg(W, 0, w.y, r);
+        W.run(kClsCoarse, 1, [&] { vec_add(w.u[w.cur], w.y, n, W.st); });
         return PMG_OK;
     }
     PLev& L = H.pl[l];
@@ -659,18 +722,83 @@ int solve_loop(pmg_work_s& W, const double* d_f, double tol, int max_cycles, dou
     if (n0 == 0.0) {
         *flags = PMG_FLAG_CONVERGED;
     } else {
-        for (int c = 1; c <= max_cycles; ++c) {
-            rc = vcycle(W, 0, d_f, w0.r, false);
-            if (rc) break;
+        // one cycle: V-cycle, then the stop-test residual (reused by the next cycle's first
+        // pre-smoothing) with rho = ||r|| / ||r0|| formed on the device
+        auto body = [&]() -> int {
+            int r = vcycle(W, 0, d_f, w0.r, false);
+            if (r) return r;
             NormCtx ncc = W.nc;
             ncc.norm_out = nullptr;
             ncc.n0 = W.norm0;
-            ncc.hist_out = W.dhist + c;
+            ncc.hist_out = W.rho_dev;
             W.run(kClsResid0, 1,
                   [&] { sell_rowop(L0.A->S, kOpResidual, w0.u[w0.cur], d_f, nullptr, w0.r, &ncc, W.st); });
-            PMG_CUDA(cudaMemcpyAsync(W.h_pinned + c, W.dhist + c, sizeof(double), cudaMemcpyDeviceToHost, W.st));
+            PMG_CUDA(cudaMemcpyAsync(W.rho_host, W.rho_dev, sizeof(double), cudaMemcpyDeviceToHost, W.st));
+            return PMG_OK;
+        };
+        const bool graphs = !W.prof && !env_flag("PMG_NO_GRAPH");
+        auto cur_mask = [&] {  // which of the two iterate buffers each p-level uses
+            int m = 0;
+            for (size_t l = 0; l < W.pw.size(); ++l) m |= W.pw[l].cur << l;
+            return m;
+        };
+        for (int c = 1; c <= max_cycles; ++c) {
+            // the first cycle of a solve runs eagerly (lazy one-time setup happens there)
+            const bool replay = graphs && W.gx && W.gx_f == d_f && W.gx_cur == cur_mask();
+            if (graphs && !replay && c >= 2) {
+                if (W.gx) cudaGraphExecDestroy(W.gx);
+                W.gx = nullptr;
+                std::vector<int> curs;
+                for (auto& pw : W.pw) curs.push_back(pw.cur);
+                const int64_t l0 = W.launches;
+                int64_t c0[kNumCls], c1[kNumCls];
+                std::copy(W.cls_launches, W.cls_launches + kNumCls, c0);
+                cudaGraph_t g = nullptr;
+                PMG_CUDA(cudaStreamBeginCapture(W.st, cudaStreamCaptureModeThreadLocal));
+                int r = PMG_OK;
+                try {
+                    r = body();
+                } catch (...) {
+                    cudaStreamEndCapture(W.st, &g);
+                    if (g) cudaGraphDestroy(g);
+                    throw;
+                }
+                const int64_t l1 = W.launches;
+                std::copy(W.cls_launches, W.cls_launches + kNumCls, c1);
+                PMG_CUDA(cudaStreamEndCapture(W.st, &g));
+                if (r) {
+                    cudaGraphDestroy(g);
+                    rc = r;
+                    break;
+                }
+                // a cycle must leave every level's buffer selection as it found it (Gauss-Seidel
+                // flips it per sweep), else the replay would read stale buffers
+                bool same = true;
+                for (size_t l = 0; l < W.pw.size(); ++l) {
+                    same = same && W.pw[l].cur == curs[l];
+                    W.pw[l].cur = curs[l];
+                }
+                W.launches = l0;  // counted per execution below
+                std::copy(c0, c0 + kNumCls, W.cls_launches);
+                if (same) {
+                    PMG_CUDA(cudaGraphInstantiate(&W.gx, g, 0));
+                    W.gx_f = d_f;
+                    W.gx_cur = cur_mask();
+                    W.gx_launches = l1 - l0;
+                    for (int k = 0; k < kNumCls; ++k) W.gx_cls[k] = c1[k] - c0[k];
+                }
+                cudaGraphDestroy(g);
+            }
+            if (graphs && W.gx && W.gx_f == d_f && W.gx_cur == cur_mask()) {
+                PMG_CUDA(cudaGraphLaunch(W.gx, W.st));
+                W.launches += W.gx_launches;
+                for (int k = 0; k < kNumCls; ++k) W.cls_launches[k] += W.gx_cls[k];
+            } else {
+                rc = body();
+                if (rc) break;
+            }
             PMG_CUDA(cudaStreamSynchronize(W.st));
-            const double rho = W.h_pinned[c];
+            const double rho = *W.rho_host;
             rho_hist[c] = rho;
             *cycles = c;
             if (rho <= tol) {
@@ -1002,10 +1130,10 @@ int pmg_factor_stats(pmg_factor F, int64_t* nnz_L, int64_t* nnz_U, int32_t* leve
 }
 
 int pmg_factor_sweep_info(pmg_factor F, int32_t* kind, int32_t* seg, int32_t* skew_D_L, int32_t* skew_D_U) {
-    if (kind) *kind = F->skew ? PMG_SWEEP_SKEW : F->seg > 0 ? PMG_SWEEP_CHAIN : PMG_SWEEP_LEVELS;
+    if (kind) *kind = F->wave ? PMG_SWEEP_WAVE : F->skew ? PMG_SWEEP_SKEW : F->seg > 0 ? PMG_SWEEP_CHAIN : PMG_SWEEP_LEVELS;
     if (seg) *seg = F->seg;
-    if (skew_D_L) *skew_D_L = F->skew ? F->planL.lead : 0;
-    if (skew_D_U) *skew_D_U = F->skew ? F->planU.lead : 0;
+    if (skew_D_L) *skew_D_L = F->wave ? F->waveL.lead : F->skew ? F->planL.lead : 0;
+    if (skew_D_U) *skew_D_U = F->wave ? F->waveU.lead : F->skew ? F->planU.lead : 0;
     return PMG_OK;
 }
 
@@ -1173,9 +1301,14 @@ int pmg_work_create(pmg_hier H, pmg_work* out) {
         const int32_t n0 = H->pl[0].A->A.n;
         W->nc.partials = dalloc<double>(ceil_div(n0, 256) + 1);
         W->nc.counter = reinterpret_cast<unsigned*>(dalloc<double>(1));
-        PMG_CUDA(cudaMemset(W->nc.counter, 0, sizeof(double)));
+        // the norm's last-block counter must be zero before the first fused residual on W->st
+        // (a non-blocking stream: order the reset on that stream and wait for it)
+        PMG_CUDA(cudaMemsetAsync(W->nc.counter, 0, sizeof(double), W->st));
         W->norm0 = dalloc<double>(1);
+        W->rho_dev = dalloc<double>(1);
+        PMG_CUDA(cudaMallocHost(&W->rho_host, sizeof(double)));
         ensure_hist(*W, 200);
+        PMG_CUDA(cudaStreamSynchronize(W->st));
         *out = W.release();
         return PMG_OK;
     });

@@ -594,25 +594,16 @@ void chain_sweep(const ChainOp& op, int* ticket, cudaStream_t st) {
     const int nseg = ceil_div(n, op.seg);
     // segment progress: the caller's scratch after the ticket (one shared spill buffer only for
     // orderings with more segments than the scratch holds)
-    static int* spill = nullptr;
-    static int spill_cap = 0;
     int* prog = ticket + 1;
+    int* spill = nullptr;  // stream-ordered, per call: concurrent sweeps share no scratch
     if (nseg >= kSweepScratchInts) {
-        if (nseg > spill_cap) {
-            cudaFree(spill);
-            PMG_CUDA(cudaMalloc(&spill, sizeof(int) * nseg));
-            spill_cap = nseg;
-        }
+        PMG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&spill), sizeof(int) * nseg, st));
         prog = spill;
     }
     PMG_CUDA(cudaMemsetAsync(prog, 0, sizeof(int) * nseg, st));
-    static int ahead = -1, gap = -1;
-    if (ahead < 0) {
-        const char* e = getenv("PMG_CHAIN_AHEAD");
-        ahead = e ? atoi(e) : 96;
-        const char* g = getenv("PMG_CHAIN_START_GAP");  // forces the gate (tuning)
-        gap = g ? atoi(g) : 0;
-    }
+    // tuning switches, read once (thread-safe static initialisation)
+    static const int ahead = env_int("PMG_CHAIN_AHEAD", 96);
+    static const int gap = env_int("PMG_CHAIN_START_GAP", 0);  // forces the gate
     ChainArgs a{};
     a.S = *op.S;
     a.diag = op.diag;
@@ -630,37 +621,17 @@ void chain_sweep(const ChainOp& op, int* ticket, cudaStream_t st) {
     a.prog = prog;
     a.ahead = ahead;
     a.bs = op.bs > 0 && op.bs <= 32 ? op.bs : 32;
-    static int cap = -1;
-    if (cap < 0) {
-        const char* e = getenv("PMG_CHAIN_GAP_CAP");
-        cap = e ? atoi(e) : 8;
-    }
+    static const int cap = env_int("PMG_CHAIN_GAP_CAP", 8);
     // a gate at the data reach would let each segment start only when its first row can
     // finish, exposing the start-up latency; capping it starts long-reach segments early
     a.start_gap = gap > 0 ? gap : op.start_gap > 0 ? std::min(op.start_gap, cap) : cap;
-    static int gate_dist = -1;
-    if (gate_dist < 0) {
-        const char* e = getenv("PMG_CHAIN_GATE_DIST");
-        gate_dist = e ? std::max(1, atoi(e)) : 3;
-    }
+    static const int gate_dist = std::max(1, env_int("PMG_CHAIN_GATE_DIST", 3));
     a.gate_dist = gate_dist;
-    static int prefetch = -1;
-    if (prefetch < 0) {
-        const char* e = getenv("PMG_CHAIN_PREFETCH");
-        prefetch = e ? atoi(e) : 1;
-    }
+    static const int prefetch = env_int("PMG_CHAIN_PREFETCH", 1);
     a.prefetch = prefetch;
-    static int pf_dist = -1;
-    if (pf_dist < 0) {
-        const char* e = getenv("PMG_CHAIN_PF_DIST");
-        pf_dist = e ? atoi(e) : 0;
-    }
+    static const int pf_dist = env_int("PMG_CHAIN_PF_DIST", 0);
     a.pf_dist = pf_dist;
-    static int stager_async = -1;
-    if (stager_async < 0) {
-        const char* e = getenv("PMG_STAGER_ASYNC");
-        stager_async = e ? atoi(e) : 1;
-    }
+    static const int stager_async = env_int("PMG_STAGER_ASYNC", 1);
     a.stager_async = stager_async;
     a.trace = nullptr;
     if (g_chain_trace_on) {
@@ -675,21 +646,15 @@ void chain_sweep(const ChainOp& op, int* ticket, cudaStream_t st) {
         a.trace = g_chain_trace;
         g_chain_trace_on = false;  // one-shot: trace the first sweep after enabling
     }
-    static int nsm = 0;
-    if (!nsm) {
-        int dev = 0;
-        PMG_CUDA(cudaGetDevice(&dev));
-        PMG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    }
-    const int grid = std::min(a.nseg, nsm);  // one CTA per SM: the finisher shares issue slots only with its helpers
+    const int grid = std::min(a.nseg, sm_count());  // one CTA per SM: the finisher shares issue slots only with its helpers
     const int smem = int(sizeof(ChainSmem));
-    static bool attr = false;
-    if (!attr) {
+    static const bool attr = [smem] {
         PMG_CUDA(cudaFuncSetAttribute(k_chain<kChainL>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         PMG_CUDA(cudaFuncSetAttribute(k_chain<kChainU>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         PMG_CUDA(cudaFuncSetAttribute(k_chain<kChainGS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        attr = true;
-    }
+        return true;
+    }();
+    (void)attr;
     switch (op.kind) {
         case kChainL: k_chain<kChainL><<<grid, NT, smem, st>>>(a); break;
         case kChainU: k_chain<kChainU><<<grid, NT, smem, st>>>(a); break;
@@ -700,6 +665,7 @@ void chain_sweep(const ChainOp& op, int* ticket, cudaStream_t st) {
         k_chain_upd<<<ceil_div(n, 256), 256, 0, st>>>(op.out, op.perm, op.upd, n);
         PMG_LAUNCH_CHECK();
     }
+    if (spill) PMG_CUDA(cudaFreeAsync(spill, st));
 }
 
 int32_t detect_segment(int32_t n, const int32_t* rp, const int32_t* col) {

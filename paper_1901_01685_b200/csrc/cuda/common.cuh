@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -106,5 +107,23 @@ __device__ __forceinline__ double warp_butterfly(double v) {
 }
 
 inline int ceil_div(int64_t a, int64_t b) { return int((a + b - 1) / b); }
+
+// integer tuning switch from the environment (read by callers into function-local statics,
+// whose initialisation is thread-safe)
+inline int env_int(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    return e ? std::atoi(e) : dflt;
+}
+
+// SM count of the current device (cached, thread-safe)
+inline int sm_count() {
+    static const int n = [] {
+        int dev = 0, v = 0;
+        PMG_CUDA(cudaGetDevice(&dev));
+        PMG_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
+        return v;
+    }();
+    return n;
+}
 
 }  // namespace pmg

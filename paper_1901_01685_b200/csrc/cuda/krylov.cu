@@ -61,7 +61,17 @@ __global__ void __launch_bounds__(kThreads) k_update_ur(double* __restrict__ u, 
     }
 }
 
+__global__ void __launch_bounds__(kThreads) k_vec_add(double* __restrict__ u, const double* __restrict__ e, int32_t n) {
+    for (int32_t i = blockIdx.x * kThreads + threadIdx.x; i < n; i += gridDim.x * kThreads) u[i] = u[i] + e[i];
+}
+
 }  // namespace
+
+void vec_add(double* u, const double* e, int32_t n, cudaStream_t st) {
+    if (n <= 0) return;
+    k_vec_add<<<grid_for(n), kThreads, 0, st>>>(u, e, n);
+    PMG_LAUNCH_CHECK();
+}
 
 void bicg_update_p(double* p, const double* r, const double* v, double beta, double omega, int32_t n, cudaStream_t st) {
     if (n <= 0) return;

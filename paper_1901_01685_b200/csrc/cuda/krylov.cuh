@@ -14,4 +14,7 @@ void bicg_update_s(double* s, const double* r, const double* v, double alpha, in
 void bicg_update_ur(double* u, double* r, const double* s, const double* t, const double* ph, const double* sh,
                     double alpha, double omega, int32_t n, cudaStream_t st);
 
+// u = u + e (the p = 1-only hierarchy's h-MG correction)
+void vec_add(double* u, const double* e, int32_t n, cudaStream_t st);
+
 }  // namespace pmg

@@ -202,8 +202,10 @@ __global__ void __launch_bounds__(NT) k_skew(SkewArgs a) {
                         __nanosleep(ns);
                         ns = min(ns * 2, 1024u);
                     }
+                    // done[far_blk] does not imply that lower source blocks have finished (a
+                    // block with no halo needs can end early): wait on every value
                     double* far = Ybase + (DM + SPW) * RYS;
-                    for (int i = lane; i < nf; i += 32) far[i] = a.out[a.far_idx[f0 + i]];
+                    for (int i = lane; i < nf; i += 32) far[i] = wait_value(a.out, a.far_idx[f0 + i]);
                     __syncwarp();
                 }
                 int f[MAXD], Rq[MAXD], Wq[MAXD];
@@ -773,13 +775,12 @@ void skew_plan_free(SkewPlan& plan) {
 namespace {
 template <int K, int NR, int C>
 void launch(const SkewArgs& a, int grid, int smem, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
+    static const bool attr = [] {
         PMG_CUDA(cudaFuncSetAttribute(k_skew<K, NR, C, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        // (GS rows hold the lower half of A's row: <= 61 terms at p = 5)
         PMG_CUDA(cudaFuncSetAttribute(k_skew<K, NR, C, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        attr = true;
-    }
+        return true;
+    }();
+    (void)attr;
     if (a.trace) k_skew<K, NR, C, true><<<grid, NT, smem, st>>>(a);
     else k_skew<K, NR, C, false><<<grid, NT, smem, st>>>(a);
     PMG_LAUNCH_CHECK();
@@ -800,12 +801,7 @@ void skew_sweep(const SkewOp& op, int* ticket, cudaStream_t st) {
     if (n == 0) return;
     fill_sentinel(op.out, n, st);
     PMG_CUDA(cudaMemsetAsync(ticket, 0, sizeof(int), st));
-    static int nsm = 0;
-    if (!nsm) {
-        int dev = 0;
-        PMG_CUDA(cudaGetDevice(&dev));
-        PMG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    }
+    const int nsm = sm_count();
     const int smem = int(smem_bytes(p.nr, p.dm, p.ry, p.nfar_max));
     // finished-block flags: the caller's scratch after the ticket (the plan's own array only for
     // factors with more blocks than the scratch holds)
@@ -825,11 +821,7 @@ void skew_sweep(const SkewOp& op, int* ticket, cudaStream_t st) {
         g_skew_trace_n = p.nblk;
         a.trace = g_skew_trace;
     }
-    static int grid_cap = -1;  // tests: fewer CTAs than blocks (CTAs then loop over blocks)
-    if (grid_cap < 0) {
-        const char* e = getenv("PMG_SKEW_GRID");
-        grid_cap = e ? std::max(1, atoi(e)) : 0;
-    }
+    static const int grid_cap = std::max(0, env_int("PMG_SKEW_GRID", 0));  // tests: fewer CTAs than blocks
     const int per_sm = std::max(1, int((227 * 1024) / (smem + 1024)));
     const int grid = std::min(std::min(p.nblk, nsm * per_sm), grid_cap > 0 ? grid_cap : INT_MAX);
     if (op.kind == kSkewL) launch_kind<kSkewL>(p, a, grid, smem, st);

@@ -1,0 +1,52 @@
+// Rotating-lane wavefront sweeps for the triangular solves and Gauss-Seidel on tensor-grid
+// orderings: the default sweep kernel for every factor whose rows
+// fit a layout.  See wave.cu for the design; skew.cu / chain.cu / trsv.cu remain as fallbacks.
+#pragma once
+
+#include "skew.cuh"
+
+namespace pmg {
+
+// Per-(block, step, lane) items (4 coefficients + 4 shared-memory byte offsets, 48 B) stored
+// step-major per warp block; a CTA runs `w` consecutive blocks (one sweep warp each).
+struct WavePlan {
+    int32_t n = 0, seg = 0, nseg = 0;
+    int32_t nr = 4, c = 3;       // lanes per segment, terms per lane and step
+    int32_t spw = 8, w = 1;      // segments per warp block, warp blocks per CTA
+    int32_t nblk = 0, ntask = 0; // warp blocks, CTA tasks
+    int32_t dm = 1;              // segments back a term reaches (halo rings)
+    int32_t ry = 256;            // ring rows per segment
+    int64_t nsteps = 0;
+    int32_t* Db = nullptr;       // [nblk] lane skew between a block's segments
+    int32_t* Lb = nullptr;       // [nblk] lead over the previous block: before step t, prog(b-1) >= t + Lb
+    int32_t* bp = nullptr;       // [nblk][w] ring back-pressure: before group q, prog(b+j) >= (q+1)G + bp
+    int32_t* hoff = nullptr;     // [ntask][8] bridge: halo row counts -> virtual progress of the previous block
+    int32_t* hrb = nullptr;      // [ntask][w][8] bridge: halo row j may be written iff j < prog(w) + hrb
+    int64_t* off = nullptr;      // [nblk+1] first step of each block in the item stream
+    uint4* item = nullptr;       // [nsteps][3][32]
+    int32_t lead = 0;            // median Lb (reporting)
+    bool ok = false;
+};
+
+// Build the plan of the v-ordered matrix S (kinds and arguments as skew_plan).  Returns false
+// (nothing allocated) if a row does not fit the widest layout, reaches more than 8 segments
+// back, or the rings do not fit shared memory.
+bool wave_plan(const Sell& S, const double* dinv, int32_t seg, SkewKind kind, int32_t max_terms, WavePlan& plan,
+               cudaStream_t st, const int32_t* nlow = nullptr);
+void wave_plan_free(WavePlan& plan);
+
+struct WaveOp {
+    SkewKind kind;
+    const WavePlan* plan;
+    const double* rhs;   // L: r; U: y; GS: f (natural order)
+    double* out;         // v-space outputs (sentinel protocol between CTAs)
+    double* upd;         // U: u[i] += x_i after the sweep
+    const Sell* gsS = nullptr;  // Gauss-Seidel: upper sums over the old values (pre-pass)
+    const int32_t* nlow = nullptr;
+    const double* old = nullptr;
+    double* su = nullptr;
+};
+
+void wave_sweep(const WaveOp& op, int* ticket, cudaStream_t st);
+
+}  // namespace pmg

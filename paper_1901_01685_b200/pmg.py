@@ -18,7 +18,9 @@ if the CUDA library cannot run, the call raises :class:`CudaError`.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes
+import threading
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -234,7 +236,7 @@ class IlutFactorization:
         return dict(nnz_L=a.value, nnz_U=b.value, levels_L=c.value, levels_U=d.value,
                     rows_per_level_L=n / max(c.value, 1), rows_per_level_U=n / max(d.value, 1),
                     max_row_L=e.value, max_row_U=f.value,
-                    sweep=("levels", "chain", "skew")[k.value], segment=sg.value, skew_D=(dl.value, du.value))
+                    sweep=("levels", "chain", "skew", "wave")[k.value], segment=sg.value, skew_D=(dl.value, du.value))
 
     def export(self):
         s = self.stats()
@@ -332,18 +334,43 @@ class PmgHierarchy:
         st = lib().pmg_hier_create(ctypes.byref(d), ctypes.byref(h), ctypes.byref(lvl), ctypes.byref(row))
         _raise(st, row.value, lvl.value, what="build_hierarchy")
         self.h = h.value
-        w = ctypes.c_void_p()
-        _raise(lib().pmg_work_create(self.h, ctypes.byref(w)), what="work_create")
-        self.w = w.value
+        # per-solve state lives in work objects (vectors, stream, scratch); the hierarchy itself
+        # is immutable, so concurrent solves from several host threads each
+        # take a work object of their own from this pool
+        self.w = self._new_work()
+        self._free = [self.w]
+        self._all = [self.w]
+        self._lock = threading.Lock()
         s = HierStats()
         lib().pmg_hier_get_stats(self.h, ctypes.byref(s))
         self.setup_seconds, self.ilut_seconds, self.device_bytes = s.setup_seconds, s.ilut_seconds, s.device_bytes
         self.nfactors = (len(pl) - 1 if smoother == "ilut" else 0) + len(hl) - 1
 
+    def _new_work(self):
+        w = ctypes.c_void_p()
+        _raise(lib().pmg_work_create(self.h, ctypes.byref(w)), what="work_create")
+        return w.value
+
+    @contextlib.contextmanager
+    def work(self):
+        """A work object for one call: the primary one when free, else a new pooled one."""
+        with self._lock:
+            w = self._free.pop() if self._free else None
+        if w is None:
+            w = self._new_work()
+            with self._lock:
+                self._all.append(w)
+        try:
+            yield w
+        finally:
+            with self._lock:
+                self._free.append(w)
+
     def __del__(self):
-        if getattr(self, "w", None):
-            lib().pmg_work_destroy(self.w)
-            self.w = None
+        for w in getattr(self, "_all", []):
+            lib().pmg_work_destroy(w)
+        self._all = []
+        self.w = None
         if getattr(self, "h", None):
             lib().pmg_hier_destroy(self.h)
             self.h = None
@@ -399,7 +426,8 @@ def restrict(hier: PmgHierarchy, level: int, r, n_coarse: int):
 
 def cycle(hier: PmgHierarchy, level: int, u, f):
     u = np.array(_f64(u), copy=True)
-    _raise(lib().pmg_cycle(hier.w, level, ptr(u), ptr(_f64(f, u.size))), what="cycle")
+    with hier.work() as w:
+        _raise(lib().pmg_cycle(w, level, ptr(u), ptr(_f64(f, u.size))), what="cycle")
     return u
 
 
@@ -409,8 +437,9 @@ def solve(hier: PmgHierarchy, f, tol=1e-8, max_cycles=200, guess=None):
     u = np.zeros(hier.n) if guess is None else np.array(_f64(guess, hier.n), copy=True)
     hist = np.zeros(max_cycles + 1)
     cyc, flags, secs = ctypes.c_int(), ctypes.c_int(), ctypes.c_double()
-    st = lib().pmg_solve(hier.w, ptr(f), ptr(u), tol, max_cycles, ptr(hist), ctypes.byref(cyc), ctypes.byref(flags),
-                         ctypes.byref(secs))
+    with hier.work() as w:
+        st = lib().pmg_solve(w, ptr(f), ptr(u), tol, max_cycles, ptr(hist), ctypes.byref(cyc), ctypes.byref(flags),
+                             ctypes.byref(secs))
     _raise(st, what="solve")
     c = cyc.value
     return u, SolveReport(c, hist[: c + 1].copy(), bool(flags.value & 1), bool(flags.value & 2), hier.setup_seconds,
@@ -424,8 +453,9 @@ def bicgstab(hier: PmgHierarchy, f, tol=1e-8, max_iter=200, guess=None):
     u = np.zeros(hier.n) if guess is None else np.array(_f64(guess, hier.n), copy=True)
     hist = np.zeros(max_iter + 1)
     it, flags, secs = ctypes.c_int(), ctypes.c_int(), ctypes.c_double()
-    st = lib().pmg_bicgstab(hier.w, ptr(f), ptr(u), tol, max_iter, ptr(hist), ctypes.byref(it), ctypes.byref(flags),
-                            ctypes.byref(secs))
+    with hier.work() as w:
+        st = lib().pmg_bicgstab(w, ptr(f), ptr(u), tol, max_iter, ptr(hist), ctypes.byref(it), ctypes.byref(flags),
+                                ctypes.byref(secs))
     _raise(st, what="bicgstab")
     k = it.value
     return u, KrylovReport(k, hist[: k + 1].copy(), bool(flags.value & 1), bool(flags.value & 2),
@@ -436,8 +466,9 @@ def bicgstab_device(hier: PmgHierarchy, d_f: int, d_u: int, tol=1e-8, max_iter=2
     """BiCGSTAB on device-resident vectors (raw device pointers)."""
     hist = np.zeros(max_iter + 1)
     it, flags, secs = ctypes.c_int(), ctypes.c_int(), ctypes.c_double()
-    st = lib().pmg_bicgstab_device(hier.w, ctypes.c_void_p(d_f), ctypes.c_void_p(d_u), tol, max_iter, ptr(hist),
-                                   ctypes.byref(it), ctypes.byref(flags), ctypes.byref(secs))
+    with hier.work() as w:
+        st = lib().pmg_bicgstab_device(w, ctypes.c_void_p(d_f), ctypes.c_void_p(d_u), tol, max_iter, ptr(hist),
+                                       ctypes.byref(it), ctypes.byref(flags), ctypes.byref(secs))
     _raise(st, what="bicgstab_device")
     k = it.value
     return KrylovReport(k, hist[: k + 1].copy(), bool(flags.value & 1), bool(flags.value & 2), bool(flags.value & 4),
@@ -448,8 +479,9 @@ def solve_device(hier: PmgHierarchy, d_f: int, d_u: int, tol=1e-8, max_cycles=20
     """Solve on device-resident vectors (raw device pointers, e.g. ``torch_tensor.data_ptr()``)."""
     hist = np.zeros(max_cycles + 1)
     cyc, flags, secs = ctypes.c_int(), ctypes.c_int(), ctypes.c_double()
-    st = lib().pmg_solve_device(hier.w, ctypes.c_void_p(d_f), ctypes.c_void_p(d_u), tol, max_cycles, ptr(hist),
-                                ctypes.byref(cyc), ctypes.byref(flags), ctypes.byref(secs))
+    with hier.work() as w:
+        st = lib().pmg_solve_device(w, ctypes.c_void_p(d_f), ctypes.c_void_p(d_u), tol, max_cycles, ptr(hist),
+                                    ctypes.byref(cyc), ctypes.byref(flags), ctypes.byref(secs))
     _raise(st, what="solve_device")
     c = cyc.value
     return SolveReport(c, hist[: c + 1].copy(), bool(flags.value & 1), bool(flags.value & 2), hier.setup_seconds,

@@ -15,17 +15,33 @@ from paper_1901_01685_b200 import problems as P
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["chain", "skew+chain", "levelsched"])
+@pytest.fixture(params=["wave", "skew", "chain", "levelsched"])
 def sweep_path(request, monkeypatch):
-    """Every sweep implementation must match the oracle: the default (skewed-warp kernel for
-    the short-row p=1 factors, chained-segment wavefront for the rest), the chained-segment
-    kernel for every factor (PMG_SKEW=0) and the level-scheduled fallback."""
+    """Every sweep implementation must match the oracle: the default rotating-lane kernel
+    (wave.cu), the skewed-warp kernel (PMG_WAVE=0), the chained-segment kernel (PMG_WAVE=0,
+    PMG_SKEW=0) and the level-scheduled fallback."""
     monkeypatch.delenv("PMG_FORCE_LEVELSCHED", raising=False)
     monkeypatch.delenv("PMG_SKEW", raising=False)
+    monkeypatch.delenv("PMG_WAVE", raising=False)
     if request.param == "levelsched":
         monkeypatch.setenv("PMG_FORCE_LEVELSCHED", "1")
     elif request.param == "chain":
+        monkeypatch.setenv("PMG_WAVE", "0")
         monkeypatch.setenv("PMG_SKEW", "0")
+    elif request.param == "skew":
+        monkeypatch.setenv("PMG_WAVE", "0")
+    return request.param
+
+
+@pytest.fixture(params=["wave", "skew"])
+def engine(request, monkeypatch):
+    """The two wavefront kernels for tensor-grid factors: rotating lanes (wave.cu, default) and
+    skewed warps (skew.cu, PMG_WAVE=0)."""
+    monkeypatch.delenv("PMG_SKEW", raising=False)
+    monkeypatch.delenv("PMG_FORCE_LEVELSCHED", raising=False)
+    monkeypatch.delenv("PMG_WAVE", raising=False)
+    if request.param == "skew":
+        monkeypatch.setenv("PMG_WAVE", "0")
     return request.param
 
 RTOL_RHO = 1e-10
@@ -137,17 +153,14 @@ def test_solve_config3(sweep_path):
 
 @pytest.mark.parametrize("h_exp", [4, 5, 6, 8])
 @pytest.mark.parametrize("geometry", ["square", "annulus"])
-def test_skew_sweeps_p1(h_exp, geometry, monkeypatch):
-    """The skewed-warp sweeps (skew.cu) on p=1 factors: one 8-segment warp block (h=2^-4:
-    17 segments -> 3 blocks), many blocks with halo hand-offs (2^-5 .. 2^-8), bitwise against
-    the oracle."""
-    monkeypatch.delenv("PMG_SKEW", raising=False)
-    monkeypatch.delenv("PMG_FORCE_LEVELSCHED", raising=False)
+def test_skew_sweeps_p1(h_exp, geometry, engine):
+    """The wavefront sweeps on p=1 factors: one 8-segment warp block (h=2^-4: 17 segments ->
+    3 blocks), many blocks with halo hand-offs (2^-5 .. 2^-8), bitwise against the oracle."""
     spec = P.make_spec(geometry=geometry, rhs="one", degrees=(2, 1), h_exp=h_exp)
     A = P.build(spec).hlevels[0].A
     Fg = pmg.ilut_factorize(A, 1e-12, 1.0, "none")
     st = Fg.stats()
-    assert st["sweep"] == "skew", st
+    assert st["sweep"] == engine, st
     Fo = O.ilut_factorize(A, 1e-12, 1.0, O.ORDER_NONE)
     rng = np.random.default_rng(h_exp)
     for _ in range(3):
@@ -155,33 +168,35 @@ def test_skew_sweeps_p1(h_exp, geometry, monkeypatch):
         assert_bitwise(pmg.ilut_apply(Fg, r), Fo.apply(r), "skew ilut_apply")
 
 
-def test_skew_sweeps_cta_loops():
-    """Fewer CTAs than warp blocks (PMG_SKEW_GRID, read once per process): CTAs claim blocks in
-    order and re-arm their barriers per block.  Run in a subprocess so the cap stays local."""
+@pytest.mark.parametrize("env", [{"PMG_WAVE": "0", "PMG_SKEW_GRID": "3"}, {"PMG_WAVE_GRID": "3"},
+                                 {"PMG_WAVE_GRID": "2", "PMG_WAVE_W": "1"}])
+def test_skew_sweeps_cta_loops(env):
+    """Fewer CTAs than warp blocks (PMG_SKEW_GRID / PMG_WAVE_GRID, read once per process): CTAs
+    claim blocks in order and re-arm their barriers per block; also one sweep warp per CTA
+    (PMG_WAVE_W=1).  Run in a subprocess so the settings stay local."""
     import os, subprocess, sys
     code = (
         "import numpy as np, sys; sys.path.insert(0, '.');"
         "from oracle import oracle as O; from paper_1901_01685_b200 import pmg, problems as P;"
         "A = P.build(P.make_spec(geometry='annulus', rhs='one', degrees=(2, 1), h_exp=7)).hlevels[0].A;"
-        "F = pmg.ilut_factorize(A, 1e-12, 1.0, 'none'); assert F.stats()['sweep'] == 'skew';"
+        "F = pmg.ilut_factorize(A, 1e-12, 1.0, 'none'); assert F.stats()['sweep'] == sys.argv[1];"
         "Fo = O.ilut_factorize(A, 1e-12, 1.0, O.ORDER_NONE);"
         "r = np.random.default_rng(3).uniform(-1, 1, A.nrows);"
         "e, eo = pmg.ilut_apply(F, r), Fo.apply(r);"
         "assert (e.view(np.uint64) == eo.view(np.uint64)).all(), 'mismatch'"
     )
-    env = dict(os.environ, PMG_SKEW_GRID="3")
+    engine = "skew" if env.get("PMG_WAVE") == "0" else "wave"
+    env = dict(os.environ, **env)
     env.pop("PMG_SKEW", None)
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    res = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True, timeout=600)
+    res = subprocess.run([sys.executable, "-c", code, engine], env=env, cwd=root, capture_output=True, text=True, timeout=600)
     assert res.returncode == 0, res.stderr[-2000:]
 
 
 @pytest.mark.parametrize("p,h_exp", [(1, 5), (2, 6), (3, 6), (4, 6), (5, 6), (5, 7)])
-def test_gs_sweep_skew_degrees(p, h_exp, monkeypatch):
-    """Gauss-Seidel through the skewed-warp kernel (lower entries as stage terms, upper sums over
-    the old values by a pre-pass) on A_p of every degree, bitwise against the oracle's sweep."""
-    monkeypatch.delenv("PMG_SKEW", raising=False)
-    monkeypatch.delenv("PMG_FORCE_LEVELSCHED", raising=False)
+def test_gs_sweep_skew_degrees(p, h_exp, engine):
+    """Gauss-Seidel through the wavefront kernels (lower entries as terms, upper sums over the
+    old values by a pre-pass) on A_p of every degree, bitwise against the oracle's sweep."""
     pb = P.build(P.make_spec(geometry="annulus", rhs="one", degrees=(max(p, 2), 1), h_exp=h_exp))
     A = pb.hlevels[0].A if p == 1 else pb.plevels[0].A
     rng = np.random.default_rng(p)
@@ -191,15 +206,13 @@ def test_gs_sweep_skew_degrees(p, h_exp, monkeypatch):
 
 
 @pytest.mark.parametrize("p", [2, 3, 4, 5])
-def test_skew_sweeps_long_rows(p, monkeypatch):
-    """The skewed-warp layouts for long rows (8x4, 16x4, 32x3, 32x4 lanes x terms; up to five
+def test_skew_sweeps_long_rows(p, engine):
+    """The wavefront layouts for long rows (8x4, 16x4, 32x3, 32x4 lanes x terms; up to five
     segments back): ilut_apply on the p-level factor, bitwise against the oracle."""
-    monkeypatch.delenv("PMG_SKEW", raising=False)
-    monkeypatch.delenv("PMG_FORCE_LEVELSCHED", raising=False)
     pb = P.build(P.make_spec(geometry="annulus", rhs="one", degrees=(p, 1), h_exp=6))
     A = pb.plevels[0].A
     Fg = pmg.ilut_factorize(A, 1e-12, 1.0, "none")
-    assert Fg.stats()["sweep"] == "skew"
+    assert Fg.stats()["sweep"] == engine
     Fo = O.ilut_factorize(A, 1e-12, 1.0, O.ORDER_NONE)
     r = np.random.default_rng(p).uniform(-1, 1, A.nrows)
     assert_bitwise(pmg.ilut_apply(Fg, r), Fo.apply(r), "skew ilut_apply")
@@ -242,3 +255,45 @@ def test_concurrent_solves_share_a_hierarchy():
         u, c = results[tag]
         assert c == ro["cycles"]
         assert_bitwise(u, uo, f"concurrent solve {tag}")
+
+
+def test_concurrent_python_solves_share_a_hierarchy():
+    """pmg.solve from two Python threads on one PmgHierarchy (ctypes releases the GIL)
+    takes a work object per call from the hierarchy's pool; both results equal the oracle."""
+    import threading
+    pb = P.build(P.make_spec(geometry="annulus", rhs="annulus", degrees=(3, 1), h_exp=6))
+    Hg = pmg.build_hierarchy(pb, smoother="ilut")
+    uo, ro = O.Hierarchy(pb, smoother=O.ILUT).solve(pb.f, pb.u0)
+    results, errors = {}, []
+
+    def run(tag):
+        try:
+            for _ in range(4):
+                u, rep = pmg.solve(Hg, pb.f, guess=pb.u0)
+            results[tag] = (u, rep.cycles)
+        except Exception as e:  # surfaced below
+            errors.append(e)
+
+    ts = [threading.Thread(target=run, args=(t,)) for t in "ab"]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
+    for tag in "ab":
+        u, c = results[tag]
+        assert c == ro["cycles"]
+        assert_bitwise(u, uo, f"python concurrent solve {tag}")
+
+
+def test_p1_only_hierarchy_converges():
+    """degrees (1,) -- the hierarchy is the h-multigrid solver alone.
+    Each cycle corrects the current iterate (e = hmg(f - A u), u += e) and converges like the
+    oracle, bit for bit."""
+    pb = P.build(P.make_spec(geometry="square", rhs="one", degrees=(1,), h_exp=5))
+    Hg = pmg.build_hierarchy(pb, smoother="ilut")
+    u, rep = pmg.solve(Hg, pb.f, guess=pb.u0)
+    uo, ro = O.Hierarchy(pb, smoother=O.ILUT).solve(pb.f, pb.u0)
+    assert ro["converged"] and rep.converged
+    assert rep.cycles == ro["cycles"] < 20
+    assert_bitwise(u, uo, "p=1-only solve")

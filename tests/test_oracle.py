@@ -231,3 +231,12 @@ def test_oracle_matches_golden(key):
     assert [float(x).hex() for x in rep["residual_history"]] == rec["residual_history"]
     import hashlib
     assert hashlib.sha256(u.tobytes()).hexdigest() == rec["u_sha256"]
+
+
+def test_p1_only_hierarchy_converges():
+    """with degrees (1,) each cycle is one h-MG V-cycle on the residual equation of the
+    current iterate, so the solve converges (before the fix u was reset to B f every cycle)."""
+    from paper_1901_01685_b200 import problems as P
+    pb = P.build(P.make_spec(geometry="square", rhs="one", degrees=(1,), h_exp=5))
+    _, rep = O.Hierarchy(pb, smoother=O.ILUT).solve(pb.f, pb.u0)
+    assert rep["converged"] and rep["cycles"] < 20, rep["cycles"]
