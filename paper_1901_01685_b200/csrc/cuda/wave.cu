@@ -126,6 +126,18 @@ __device__ __forceinline__ int ld_vol_s(unsigned a) {
 __device__ __forceinline__ void st_vol_s(unsigned a, int v) {
     asm volatile("st.volatile.shared.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
+// spin (warp-uniform) until the shared counter at addr reaches need; pv: last value seen
+__device__ __forceinline__ int wait_ge(unsigned addr, int pv, int need) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "L:\n\tsetp.ge.s32 p, %0, %2;\n\t@p bra.uni D;\n\t"
+        "ld.volatile.shared.b32 %0, [%1];\n\tbra.uni L;\n"
+        "D:\n\t}"
+        : "+r"(pv)
+        : "r"(addr), "r"(need)
+        : "memory");
+    return pv;
+}
 __device__ __forceinline__ void bar_init(unsigned b, unsigned count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b), "r"(count) : "memory");
 }
@@ -356,11 +368,10 @@ __global__ void __launch_bounds__(32 * (WMAX + 2)) k_wave(WaveArgs a) {
 #pragma unroll
             for (int u = 0; u < G; ++u) {
                 const int t = tb + u;
-                if (pv < t + Lw) {
-                    do {
-                        pv = ld_vol_s(pred);
-                    } while (pv < t + Lw);
-                }
+                // the predecessor's progress, loaded a step ago (progress only grows, so a stale
+                // value is a valid lower bound); reloaded now for the next step's test, off the chain
+                pv = wait_ge(pred, pv, t + Lw);
+                pv = ld_vol_s(pred);
                 const double xb = __shfl_sync(FULL, x, gbase + ((u + c0) & (NR - 1)));
                 if (u == G - 2) group_wait(qg + 1);
                 double yn[4];
@@ -386,7 +397,6 @@ __global__ void __launch_bounds__(32 * (WMAX + 2)) k_wave(WaveArgs a) {
                 }
                 acc = stage0 ? 0.0 : r;
                 st_vol_s(s_me, t + 1);
-                pv = ld_vol_s(pred);
 #pragma unroll
                 for (int q = 0; q < 4; ++q) yc[q] = yn[q];
                 now = cur;
