@@ -149,6 +149,8 @@ int pmg_work_kernel_times(pmg_work W, double* ms_by_class, int n_classes);
 int pmg_debug_chain_trace(int mode, unsigned long long* out, int cap);
 /* the same for the skewed-warp sweeps: 4 u64 per 32-segment warp block */
 int pmg_debug_skew_trace(int mode, unsigned long long* out, int cap);
+/* the same for the rotating-lane sweeps: 4 u64 per warp block */
+int pmg_debug_wave_trace(int mode, unsigned long long* out, int cap);
 
 #ifdef __cplusplus
 }

@@ -22,7 +22,9 @@ _libs: dict[str, ctypes.CDLL] = {}
 def load(name: str) -> ctypes.CDLL:
     lib = _libs.get(name)
     if lib is None:
-        path = os.path.join(LIBDIR, name)
+        # experiments: PMG_CUDA_LIB selects an alternative build of the CUDA library in LIBDIR
+        alt = os.environ.get("PMG_CUDA_LIB") if name == "libpmg_cuda.so" else None
+        path = os.path.join(LIBDIR, alt or name)
         if not os.path.exists(path):
             raise RuntimeError(f"{path} is missing -- run `make` (or __graft_entry__.build())")
         lib = ctypes.CDLL(path, mode=ctypes.RTLD_GLOBAL)

@@ -1461,6 +1461,19 @@ int pmg_debug_skew_trace(int mode, unsigned long long* out, int cap) {
     return g_skew_trace_n;
 }
 
+// diagnostics: the same for the rotating-lane sweeps (4 u64 per warp block); returns #blocks
+int pmg_debug_wave_trace(int mode, unsigned long long* out, int cap) {
+    if (mode == 1 || mode == 0) {
+        g_wave_trace_on = mode == 1;
+        return 0;
+    }
+    if (!g_wave_trace || !out) return 0;
+    const int n = std::min(g_wave_trace_n * 4, cap);
+    if (cudaDeviceSynchronize() != cudaSuccess) return -1;
+    if (cudaMemcpy(out, g_wave_trace, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+    return g_wave_trace_n;
+}
+
 // ms_by_class[0..6]: resid(A_p), L-solve(p), U-solve(p), GS(p), p-transfers, coarse (p<finest and
 // h-MG), misc; [7] = total launches, [8..14] = launches per class.  enable: n_classes < 0 turns
 // profiling on (-1) / off (-2) and resets the counters.

@@ -47,6 +47,14 @@ constexpr int STEP_BYTES = 3 * 32 * 16;
 constexpr int MAXD = 8;         // segments back a term may reach
 constexpr int EMAX = 8;         // blocks back a term may reach
 constexpr int WMAX = 2;         // sweep warps per CTA
+#ifndef PMG_WAVE_CHK
+#define PMG_WAVE_CHK 2
+#endif
+// steps per progress test / publication: a test is a branch, which splits the unrolled step
+// sequence into basic blocks the scheduler cannot overlap; testing every CHK steps (for the
+// needs of all CHK) costs at most CHK-1 steps of extra lag per warp hand-off
+constexpr int CHK = PMG_WAVE_CHK;
+static_assert(G % CHK == 0, "CHK divides the group");
 constexpr int INF = INT_MAX / 2;
 constexpr unsigned FULL = 0xffffffffu;
 
@@ -99,8 +107,11 @@ struct WaveArgs {
     const int32_t* bp;
     const int32_t* hoff;
     const int32_t* hrb;
+    const int32_t* hsl;
     const int64_t* off;
     int32_t n, seg, nseg, nblk, ntask, W, dm, ry;
+    unsigned sbase;  // shared-window address of the dynamic shared memory the items were built for
+    unsigned long long* trace;  // diagnostics (null: off): per block [start, step 200, end, task]
     Layout lay;
     int* ticket;
 };
@@ -157,6 +168,11 @@ __device__ __forceinline__ void bar_wait(unsigned b, unsigned parity) {
         "r"(parity)
         : "memory");
 }
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 __device__ __forceinline__ double u2d(unsigned lo, unsigned hi) { return __hiloint2double(int(hi), int(lo)); }
 
 struct Step {  // a lane's item of one step
@@ -181,6 +197,7 @@ __global__ void __launch_bounds__(32 * (WMAX + 2)) k_wave(WaveArgs a) {
     constexpr int DS = 4 - C;  // first used slot; U / GS chunk 0: 1/diagonal there
     extern __shared__ __align__(128) unsigned char wave_smem[];
     const unsigned sb = smem_u32(wave_smem);
+    if (sb != a.sbase) __trap();  // the items hold absolute shared-memory addresses
     const Layout& ly = a.lay;
     const int W = a.W, DM = a.dm, RY = a.ry, RYS = a.ry + 1;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -257,11 +274,12 @@ __global__ void __launch_bounds__(32 * (WMAX + 2)) k_wave(WaveArgs a) {
         if (warp == W + 1) {
             // ------------------------------------------------------------ bridge
             // halo segment g0-1-d (d < DM) -> ring d' = DM-1-d; vprog = min_d (f[d] + hoff[d])
-            int f[MAXD], ho[MAXD], rows[MAXD], hr[WMAX][MAXD];
+            int f[MAXD], ho[MAXD], rows[MAXD], hr[WMAX][MAXD], sl[MAXD];
 #pragma unroll
             for (int d = 0; d < MAXD; ++d) {
                 const int gh = g0 - 1 - d;
                 ho[d] = d < DM ? a.hoff[task * MAXD + d] : INT_MIN;
+                sl[d] = d < DM ? a.hsl[task * MAXD + d] : 0;  // ring slot of row j: (j + sl) mod RY
                 rows[d] = gh >= 0 ? int(min(int64_t(S), int64_t(n) - int64_t(gh) * S)) : 0;
                 f[d] = (d < DM && gh >= 0 && ho[d] > INT_MIN / 2) ? 0 : rows[d];
                 for (int w = 0; w < WMAX; ++w) hr[w][d] = (w < W && d < DM) ? a.hrb[(task * W + w) * MAXD + d] : INF;
@@ -287,7 +305,7 @@ __global__ void __launch_bounds__(32 * (WMAX + 2)) k_wave(WaveArgs a) {
                     if (f[d] < rows[d]) {
                         const unsigned ok = __ballot_sync(FULL, !is_sentinel(v[d]));
                         const int cnt = ok == FULL ? 32 : __ffs(~ok) - 1;
-                        if (lane < cnt) rings[(DM - 1 - d) * RYS + ((f[d] + lane) & (RY - 1))] = v[d];
+                        if (lane < cnt) rings[(DM - 1 - d) * RYS + ((f[d] + lane + sl[d]) & (RY - 1))] = v[d];
                         f[d] += cnt;
                         if (f[d] < rows[d]) vp = min(vp, f[d] + ho[d]);
                     }
@@ -320,7 +338,7 @@ __global__ void __launch_bounds__(32 * (WMAX + 2)) k_wave(WaveArgs a) {
         const int phase = (P + D * k + rl) % NR;         // lane finalises at step t <=> t % NR == phase
         const int c0 = ((-1 - P - D * k) % NR + NR) % NR;  // finaliser of step t-1: gbase + ((t + c0) % NR)
         const unsigned pred = warp == 0 ? s_vprog : s_prog + 4 * (warp - 1);
-        const unsigned XB = unsigned(ly.xb);
+        const unsigned XB = sb + unsigned(ly.xb);
         const int myring = (DM + warp * SPW + k) * RYS;  // own ring (element index)
         const unsigned ibase = sb + ly.item + warp * PF * STEP_BYTES + lane * 16;
         const unsigned rbase = sb + ly.rhs + warp * NRH * G * SPW * 8 + k * 8;
@@ -357,26 +375,34 @@ __global__ void __launch_bounds__(32 * (WMAX + 2)) k_wave(WaveArgs a) {
         fetch_item(ibase + STEP_BYTES, cur);
         double yc[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) yc[q] = lds_f64(sb + now.o[q]);
+        for (int q = 0; q < 4; ++q) yc[q] = lds_f64(now.o[q]);
         double rh = lds_f64(rbase), sr = 0.0;
         if (K == kSkewGS) sr = lds_f64(sbase2);
         double acc = 0.0, x = 0.0;
         double* outp = a.out + lo;
         backpressure(0);
+        if (a.trace && lane == 0) {
+            a.trace[b * 4 + 0] = gtimer();
+            a.trace[b * 4 + 3] = task;
+        }
         for (int tb = 0; tb < NS; tb += G) {
             const int qg = tb / G;
+            const int rgb = myring + (tb & (RY - 1));  // ring cell of step tb (RY is a multiple of G)
+            if (tb == 192 && a.trace && lane == 0) a.trace[b * 4 + 1] = gtimer();
 #pragma unroll
             for (int u = 0; u < G; ++u) {
                 const int t = tb + u;
                 // the predecessor's progress, loaded a step ago (progress only grows, so a stale
                 // value is a valid lower bound); reloaded now for the next step's test, off the chain
-                pv = wait_ge(pred, pv, t + Lw);
-                pv = ld_vol_s(pred);
+                if (u % CHK == 0) {  // one test covers the loads of steps t .. t+CHK-1
+                    pv = wait_ge(pred, pv, t + CHK - 1 + Lw);
+                    pv = ld_vol_s(pred);
+                }
                 const double xb = __shfl_sync(FULL, x, gbase + ((u + c0) & (NR - 1)));
                 if (u == G - 2) group_wait(qg + 1);
                 double yn[4];
 #pragma unroll
-                for (int q = DS; q < 4; ++q) yn[q] = lds_f64(sb + cur.o[q]);
+                for (int q = DS; q < 4; ++q) yn[q] = lds_f64(cur.o[q]);
                 fetch_item(ibase + ((t + 2) % PF) * STEP_BYTES, nxt);
                 const int rs = ((t + 1) % (NRH * G)) * SPW * 8;
                 const double rhn = lds_f64(rbase + rs);
@@ -391,12 +417,12 @@ __global__ void __launch_bounds__(32 * (WMAX + 2)) k_wave(WaveArgs a) {
                 const bool stage0 = (u & (NR - 1)) == phase;
                 const int ix = t - P - D * k;
                 x = K == kSkewL ? rh - r : K == kSkewU ? (rh - r) * now.w[DS] : ((rh - r) - sr) * now.w[DS];
-                if (stage0 && ix >= 0 && ix < rows) {
-                    rings[myring + (ix & (RY - 1))] = x;
-                    outp[ix] = x;
-                }
+                // ring cells are indexed by the step that finalised the value (cells of
+                // rows outside the segment are never read); the output only for real rows
+                if (stage0) rings[rgb + u] = x;
+                if (stage0 && ix >= 0 && ix < rows) outp[ix] = x;
                 acc = stage0 ? 0.0 : r;
-                st_vol_s(s_me, t + 1);
+                if (u % CHK == CHK - 1) st_vol_s(s_me, t + 1);
 #pragma unroll
                 for (int q = 0; q < 4; ++q) yc[q] = yn[q];
                 now = cur;
@@ -409,6 +435,7 @@ __global__ void __launch_bounds__(32 * (WMAX + 2)) k_wave(WaveArgs a) {
             refill(qg + NG);
             backpressure(qg + 1);
         }
+        if (a.trace && lane == 0) a.trace[b * 4 + 2] = gtimer();
         // finished: no ring cell is read any more; "done" is published once the predecessor is
         // done (keeps the progress chain valid)
         st_vol_s(sb + ly.rdp + 4 * warp, INF);
@@ -528,8 +555,8 @@ __global__ void k_wave_req2(Sell S, const int32_t* nlow, int32_t seg, int NR, in
 template <int K>
 __global__ void k_wave_fill(Sell S, const int32_t* __restrict__ nlow, const double* __restrict__ dinv, int32_t seg,
                             int32_t nseg, const int32_t* __restrict__ Db, const int64_t* __restrict__ off, int32_t nblk,
-                            int NR, int C, int W, int DM, int RY, int ring0, int xb, int64_t nsteps,
-                            uint4* __restrict__ item) {
+                            int NR, int C, int W, int DM, int RY, int ring0, int xb, unsigned sbase,
+                            int64_t nsteps, uint4* __restrict__ item) {
     const int64_t gid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (gid >= nsteps * 32) return;
     const int64_t ts = gid >> 5;
@@ -549,7 +576,7 @@ __global__ void k_wave_fill(Sell S, const int32_t* __restrict__ nlow, const doub
     const int s = ((rl - base) % NR + NR) % NR;
     const int ix = base + s;           // the row this lane works on (chunk s)
     const int RYS = RY + 1;
-    const int zero = ring0 + 8 * RY;
+    const unsigned zero = sbase + ring0 + 8 * RY;
     Step it;
     for (int q = 0; q < 4; ++q) {
         it.w[q] = 0.0;
@@ -567,10 +594,11 @@ __global__ void k_wave_fill(Sell S, const int32_t* __restrict__ nlow, const doub
             const int gc = c / seg, jx = c - gc * seg, d = g - gc;
             it.w[q] = r.val(i);
             if (d == 0 && q == 3 && jx == ix - s - 1) {
-                it.o[q] = unsigned(xb);
-            } else {
+                it.o[q] = sbase + unsigned(xb);
+            } else {  // the cell of the step that finalised row jx of segment gc
                 const int ridx = DM + (gc - g0);
-                it.o[q] = unsigned(ring0 + 8 * (ridx * RYS + (jx & (RY - 1))));
+                const int pstep = jx + P + Db[gc / SPW] * (gc % SPW);
+                it.o[q] = sbase + unsigned(ring0 + 8 * (ridx * RYS + (pstep & (RY - 1))));
             }
         }
     }
@@ -617,6 +645,28 @@ void launch_req(const Sell& S, const int32_t* nlow, int32_t seg, int NR, int C, 
     PMG_LAUNCH_CHECK();
 }
 
+__global__ void k_sbase(unsigned* out) {
+    extern __shared__ __align__(128) unsigned char probe_smem[];
+    *out = smem_u32(probe_smem);
+}
+
+// shared-window address of a kernel's dynamic shared memory (no static shared memory, no
+// cluster): the items are built with it, k_wave checks it
+unsigned dyn_smem_base(cudaStream_t st) {
+    static const unsigned base = [st] {
+        unsigned* d = nullptr;
+        unsigned h = 0;
+        PMG_CUDA(cudaMalloc(&d, sizeof(unsigned)));
+        k_sbase<<<1, 32, 128, st>>>(d);
+        PMG_LAUNCH_CHECK();
+        PMG_CUDA(cudaMemcpyAsync(&h, d, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+        PMG_CUDA(cudaStreamSynchronize(st));
+        cudaFree(d);
+        return h;
+    }();
+    return base;
+}
+
 int smem_limit() {
     static const int lim = [] {
         int dev = 0, v = 0;
@@ -628,6 +678,10 @@ int smem_limit() {
 }
 
 }  // namespace
+
+bool g_wave_trace_on = false;
+unsigned long long* g_wave_trace = nullptr;
+int g_wave_trace_n = 0;
 
 bool wave_plan(const Sell& S, const double* dinv, int32_t seg, SkewKind kind, int32_t max_terms, WavePlan& plan,
                cudaStream_t st, const int32_t* nlow) {
@@ -740,13 +794,15 @@ bool wave_plan(const Sell& S, const double* dinv, int32_t seg, SkewKind kind, in
             if (Wv > INT_MIN) hbp[size_t(b) * W + j] = Wv - ry;
         }
     // bridge data per CTA task and halo distance
-    std::vector<int32_t> hho(size_t(ntask) * MAXD, INT_MIN), hhr(size_t(ntask) * W * MAXD, INF);
+    std::vector<int32_t> hho(size_t(ntask) * MAXD, INT_MIN), hhr(size_t(ntask) * W * MAXD, INF),
+        hsl(size_t(ntask) * MAXD, 0);
     for (int tk = 0; tk < ntask; ++tk) {
         const int b0 = tk * W, g0 = b0 * SPW;
         for (int d = 0; d < dm; ++d) {
             const int gh = g0 - 1 - d;
             if (gh < 0) continue;
             const int bpd = gh / SPW, kp = gh % SPW, e = b0 - bpd;
+            hsl[size_t(tk) * MAXD + d] = int32_t(P + int64_t(hD[bpd]) * kp);
             bool used = false;
             for (int w = 0; w < W && b0 + w < nblk; ++w) {
                 const int ee = e + w;
@@ -774,13 +830,15 @@ bool wave_plan(const Sell& S, const double* dinv, int32_t seg, SkewKind kind, in
     const int64_t nsteps = hoff[nblk];
     std::vector<int32_t> hL(nblk);
     for (int b = 0; b < nblk; ++b) hL[b] = int32_t(std::min<int64_t>(Lb[b], INF));
-    int32_t *Lbd = nullptr, *bpd = nullptr, *hod = nullptr, *hrd = nullptr;
+    int32_t *Lbd = nullptr, *bpd = nullptr, *hod = nullptr, *hrd = nullptr, *hsd = nullptr;
     int64_t* offd = nullptr;
     uint4* item = nullptr;
     PMG_CUDA(cudaMalloc(&Lbd, sizeof(int32_t) * nblk));
     PMG_CUDA(cudaMalloc(&bpd, sizeof(int32_t) * hbp.size()));
     PMG_CUDA(cudaMalloc(&hod, sizeof(int32_t) * hho.size()));
     PMG_CUDA(cudaMalloc(&hrd, sizeof(int32_t) * hhr.size()));
+    PMG_CUDA(cudaMalloc(&hsd, sizeof(int32_t) * hsl.size()));
+    PMG_CUDA(cudaMemcpyAsync(hsd, hsl.data(), sizeof(int32_t) * hsl.size(), cudaMemcpyHostToDevice, st));
     PMG_CUDA(cudaMalloc(&offd, sizeof(int64_t) * (nblk + 1)));
     PMG_CUDA(cudaMalloc(&item, size_t(nsteps) * STEP_BYTES));
     PMG_CUDA(cudaMemcpyAsync(Lbd, hL.data(), sizeof(int32_t) * nblk, cudaMemcpyHostToDevice, st));
@@ -789,15 +847,16 @@ bool wave_plan(const Sell& S, const double* dinv, int32_t seg, SkewKind kind, in
     PMG_CUDA(cudaMemcpyAsync(hrd, hhr.data(), sizeof(int32_t) * hhr.size(), cudaMemcpyHostToDevice, st));
     PMG_CUDA(cudaMemcpyAsync(offd, hoff.data(), sizeof(int64_t) * (nblk + 1), cudaMemcpyHostToDevice, st));
     const int nf = ceil_div(nsteps * 32, 256);
+    const unsigned sbase = dyn_smem_base(st);
     if (kind == kSkewL)
         k_wave_fill<kSkewL><<<nf, 256, 0, st>>>(S, nlow, dinv, seg, nseg, p.Db, offd, nblk, NR, C, W, dm, ry, ly.ring,
-                                                ly.xb, nsteps, item);
+                                                ly.xb, sbase, nsteps, item);
     else if (kind == kSkewU)
         k_wave_fill<kSkewU><<<nf, 256, 0, st>>>(S, nlow, dinv, seg, nseg, p.Db, offd, nblk, NR, C, W, dm, ry, ly.ring,
-                                                ly.xb, nsteps, item);
+                                                ly.xb, sbase, nsteps, item);
     else
         k_wave_fill<kSkewGS><<<nf, 256, 0, st>>>(S, nlow, dinv, seg, nseg, p.Db, offd, nblk, NR, C, W, dm, ry,
-                                                 ly.ring, ly.xb, nsteps, item);
+                                                 ly.ring, ly.xb, sbase, nsteps, item);
     PMG_LAUNCH_CHECK();
     PMG_CUDA(cudaStreamSynchronize(st));
     cudaFree(p.R);
@@ -822,6 +881,8 @@ bool wave_plan(const Sell& S, const double* dinv, int32_t seg, SkewKind kind, in
     plan.bp = bpd;
     plan.hoff = hod;
     plan.hrb = hrd;
+    plan.hsl = hsd;
+    plan.sbase = sbase;
     plan.off = offd;
     plan.item = item;
     plan.lead = sl.empty() ? hL[0] : sl[sl.size() / 2];
@@ -838,6 +899,7 @@ void wave_plan_free(WavePlan& plan) {
     cudaFree(plan.bp);
     cudaFree(plan.hoff);
     cudaFree(plan.hrb);
+    cudaFree(plan.hsl);
     cudaFree(plan.off);
     cudaFree(plan.item);
     plan = WavePlan{};
@@ -885,6 +947,17 @@ void wave_sweep(const WaveOp& op, int* ticket, cudaStream_t st) {
     a.bp = p.bp;
     a.hoff = p.hoff;
     a.hrb = p.hrb;
+    a.hsl = p.hsl;
+    a.sbase = p.sbase;
+    a.trace = nullptr;
+    if (g_wave_trace_on) {  // one-shot trace of the next sweep (diagnostics)
+        g_wave_trace_on = false;
+        cudaFree(g_wave_trace);
+        PMG_CUDA(cudaMalloc(&g_wave_trace, sizeof(unsigned long long) * 4 * p.nblk));
+        PMG_CUDA(cudaMemsetAsync(g_wave_trace, 0, sizeof(unsigned long long) * 4 * p.nblk, st));
+        g_wave_trace_n = p.nblk;
+        a.trace = g_wave_trace;
+    }
     a.off = p.off;
     a.n = n;
     a.seg = p.seg;

@@ -25,6 +25,25 @@ __device__ __forceinline__ double lds(unsigned a) {
     asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
     return v;
 }
+__device__ __forceinline__ int ld_vol(unsigned a) {
+    int v;
+    asm volatile("ld.volatile.shared.b32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_vol(unsigned a, int v) {
+    asm volatile("st.volatile.shared.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ int wait_ge(unsigned addr, int pv, int need) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "L:\n\tsetp.ge.s32 p, %0, %2;\n\t@p bra.uni D;\n\t"
+        "ld.volatile.shared.b32 %0, [%1];\n\tbra.uni L;\n"
+        "D:\n\t}"
+        : "+r"(pv)
+        : "r"(addr), "r"(need)
+        : "memory");
+    return pv;
+}
 __device__ __forceinline__ void sts_if(unsigned a, double v, bool p) {
     asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.shared.f64 [%0], %1;\n\t}" ::"r"(a), "d"(v),
                  "r"(int(p)));
@@ -45,6 +64,7 @@ __global__ void k(const Item* gitems, double* out, long long* cyc, int steps) {
     const unsigned ybase = smem_u32(Y);
     for (int i = lane; i < NS * 32; i += 32) {
         Item it = gitems[i];
+        if (V == 9) for (int q = 0; q < 4; ++q) it.o[q] = uint32_t(-(RY + 1) * (q % 3) + ((i % 32) * 16 + q) % RY);
         for (int q = 0; q < 4; ++q) it.o[q] = ybase + 8 * ((4 + (i % 32) / NR) * (RY + 1) + it.o[q]);
         items[i / 32][i % 32] = it;
     }
@@ -72,11 +92,20 @@ __global__ void k(const Item* gitems, double* out, long long* cyc, int steps) {
     unsigned o3 = items[0][lane].o[3];
     double rh = rhs[0][kseg];
     double* og = out + 1024 * kseg;
+    __shared__ int prog[4];
+    const unsigned progaddr = smem_u32(prog);
+    if (lane == 0) prog[0] = 0;
+    __syncwarp();
+    int pv = 0;
     long long t0 = clock64();
     for (int tb = 0; tb < steps; tb += U) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int t = tb + u;
+            if (V >= 8) {
+                pv = wait_ge(progaddr, pv, t - 5);
+                pv = ld_vol(progaddr);
+            }
             const int fsrc = gbase + ((c0 + u + NR - 1) & (NR - 1));  // finaliser of step t-1
             const double xb = __shfl_sync(FULL, x, fsrc);
             double yn[4];
@@ -110,11 +139,15 @@ __global__ void k(const Item* gitems, double* out, long long* cyc, int steps) {
                 const unsigned a = fin ? ring + 8 * ((t - P) & (RY - 1)) : dummy;
                 asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(x));
                 if (fin) og[(t - P) & 1023] = x;
+            } else if (V == 8 || V == 9) {
+                if (fin) og[(t - P) & 1023] = x;
+                if (fin) Yd[(ring - ybase) / 8 + ((t - P) & (RY - 1))] = x;
             } else if (V == 7) {
                 const unsigned a = fin ? ring + 8 * ((t - P) & (RY - 1)) : dummy;
                 asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(x));
             }
             acc = fin ? 0.0 : a;
+            if (V >= 8) st_vol(progaddr, t + 1);
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 yc[q] = yn[q];
@@ -163,6 +196,9 @@ int main() {
         k<32, 4, 32, 5, false><<<1, 32>>>(d, o, c + 9, steps);
         k<32, 4, 32, 6, false><<<1, 32>>>(d, o, c + 10, steps);
         k<32, 4, 32, 7, false><<<1, 32>>>(d, o, c + 11, steps);
+        k<32, 4, 32, 8, false><<<1, 32>>>(d, o, c + 12, steps);
+        k<32, 4, 32, 9, false><<<1, 32>>>(d, o, c + 13, steps);
+        k<32, 4, 32, 8, true><<<1, 32>>>(d, o, c + 14, steps);
         cudaDeviceSynchronize();
     }
     printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
@@ -171,5 +207,7 @@ int main() {
            c[4] / double(steps), c[5] / double(steps));
     printf("32x4 L: V2 sts_if %.1f | V3 if-stg weak %.1f | V4 if both %.1f | V5 sel-sts+stg_if %.1f | V6 sel-sts+if-stg %.1f | V7 sel-sts only %.1f\n",
            c[6] / double(steps), c[7] / double(steps), c[8] / double(steps), c[9] / double(steps), c[10] / double(steps), c[11] / double(steps));
+    printf("32x4: V8 = V4 + progress check/publish %.1f | V9 = V8 + 16-way-ish conflicts %.1f | V8 U %.1f\n",
+           c[12] / double(steps), c[13] / double(steps), c[14] / double(steps));
     return 0;
 }
