@@ -28,9 +28,9 @@ $(LIBDIR)/libiga_host.so: $(HOST_SRC) $(wildcard $(PKG)/csrc/host/*.hpp) include
 	@mkdir -p $(LIBDIR)
 	$(CXX) $(CXXFLAGS) -shared -o $@ $(HOST_SRC) -lpthread
 
-$(LIBDIR)/libiga_pmg.so: $(API_SRC) include/iga/pmg.hpp include/pmg_cuda.h $(LIBDIR)/libpmg_cuda.so
+$(LIBDIR)/libiga_pmg.so: $(API_SRC) include/iga/pmg.hpp include/pmg_cuda.h include/iga_host.h $(LIBDIR)/libpmg_cuda.so $(LIBDIR)/libiga_host.so
 	@mkdir -p $(LIBDIR)
-	$(CXX) $(CXXFLAGS) -Iinclude -shared -o $@ $(API_SRC) -L$(LIBDIR) -lpmg_cuda -Wl,-rpath,'$$ORIGIN'
+	$(CXX) $(CXXFLAGS) -Iinclude -shared -o $@ $(API_SRC) -L$(LIBDIR) -lpmg_cuda -liga_host -Wl,-rpath,'$$ORIGIN'
 
 oracle:
 	$(MAKE) -C oracle

@@ -33,7 +33,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--impl", choices=["ours", "reference", "selftest"], default="ours")
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--degree", type=int, default=0)
     ap.add_argument("--smoother", choices=["ilut", "gs"], default="ilut")
@@ -44,16 +44,40 @@ def parse():
     return ap.parse_args()
 
 
-def dist_init(n_gpus):
+def _free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def self_launch(n_gpus):
+    """`python bench.py --gpus N` without a launcher: re-run this script under torchrun, one rank
+    per GPU (the driver's form for N > 1 sets WORLD_SIZE itself and never comes here)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n_gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd, env=dict(os.environ, PMG_BENCH_LAUNCHED="1")))
+
+
+def dist_init(n_gpus, collectives=True):
+    """One process per GPU: rank / world from the launcher's environment; NCCL on GPUs, gloo on
+    CPU-only hosts (tests).  Each rank gets its own device and a share of the host threads."""
     ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws == 1 and n_gpus > 1 and not os.environ.get("PMG_BENCH_LAUNCHED"):
+        self_launch(n_gpus)
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if ws > 1:
+    if ws > 1 and collectives:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local)
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     return ws, rank, local
 
 
@@ -168,11 +192,29 @@ def run_reference(args, ws, rank):
     print(json.dumps(line), flush=True)
 
 
+def selftest(args, ws, rank):
+    """CPU check of the multi-rank plumbing (tests/test_bench_launch.py): every rank reports a
+    synthetic replica (rank r: (r+1) x 1000 DOF-iterations in (r+1) s); the job throughput is the
+    sum over ranks / the max time over ranks, printed by rank 0 as the bench line would be."""
+    from paper_1901_01685_b200.replicas import job_throughput
+    barrier(ws)
+    value, units, secs = job_throughput(1000.0 * (rank + 1), float(rank + 1))
+    barrier(ws)
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+                          "warmup": args.warmup, "impl": "selftest", "units": units, "seconds": secs,
+                          "host_threads_per_rank": max(1, (os.cpu_count() or 1) // ws)}), flush=True)
+
+
 def main():
     args = parse()
-    ws, rank, local = dist_init(args.gpus)
+    # the reference arm runs on rank 0 alone (no collectives); ours / selftest reduce over ranks
+    ws, rank, local = dist_init(args.gpus, collectives=args.impl != "reference")
     if args.impl == "reference":
         run_reference(args, ws, rank)
+        return
+    if args.impl == "selftest":
+        selftest(args, ws, rank)
         return
     import torch
 

@@ -15,6 +15,7 @@
 #include <string>
 #include <vector>
 
+#include "../iga_host.h"
 #include "../pmg_cuda.h"
 
 namespace iga {
@@ -123,7 +124,7 @@ class PmgHierarchy {  // SPEC.md:313-316, immutable after construction
     std::int32_t n_ = 0;
     std::vector<std::int32_t> sizes_;
     friend Vector prolongate(const PmgHierarchy&, int, const Vector&);
-    friend Vector restrict_(const PmgHierarchy&, int, const Vector&);
+    friend Vector restrict(const PmgHierarchy&, int, const Vector&);
     friend void cycle(const PmgHierarchy&, int, Vector&, const Vector&);
     friend std::pair<Vector, SolveReport> solve(const PmgHierarchy&, const Vector&, double, int, const Vector*);
     friend std::pair<Vector, KrylovReport> bicgstab(const PmgHierarchy&, const Vector&, double, int, const Vector*);
@@ -132,8 +133,24 @@ class PmgHierarchy {  // SPEC.md:313-316, immutable after construction
 PmgHierarchy build_hierarchy(const HierarchyInputs& in, Smoother smoother = Smoother::ilut, int nu1 = 1, int nu2 = 1,
                              double tau = 1e-12, double fillfactor = 1.0,
                              Ordering ordering = Ordering::none);
+
+// The problem side of SPEC.md:327's build_hierarchy(spec, p, h, ...): the benchmark / geometry,
+// coefficients, degree list and h of iga_problem_spec (include/iga_host.h), assembled on the
+// host by libiga_host.so (input generation, not the solve path).
+using ProblemSpec = iga_problem_spec;
+struct Problem {
+    HierarchyInputs inputs;
+    Vector f, u0;  // load vector and initial guess
+};
+ProblemSpec config_spec(int config, int degree = 0);  // BASELINE.json config 1..5 (degree: config 2's p)
+Problem assemble(const ProblemSpec& spec);
+// assemble + build_hierarchy in one call (build_hierarchy(spec, p, h, smoother, nu1, nu2))
+PmgHierarchy build_hierarchy(const ProblemSpec& spec, Smoother smoother = Smoother::ilut, int nu1 = 1, int nu2 = 1,
+                             double tau = 1e-12, double fillfactor = 1.0, Ordering ordering = Ordering::none);
 Vector prolongate(const PmgHierarchy& H, int level, const Vector& v_coarse);
-Vector restrict_(const PmgHierarchy& H, int level, const Vector& r_fine);        // SPEC.md:345-353 (`restrict` is a C keyword)
+Vector restrict(const PmgHierarchy& H, int level, const Vector& r_fine);
+// (`restrict` is a C99 keyword, not a C++ one; the former spelling stays as an alias)
+inline Vector restrict_(const PmgHierarchy& H, int level, const Vector& r_fine) { return restrict(H, level, r_fine); }
 void cycle(const PmgHierarchy& H, int level, Vector& u, const Vector& f);
 // SPEC.md:363-371; guess == nullptr -> zero initial guess
 std::pair<Vector, SolveReport> solve(const PmgHierarchy& H, const Vector& f, double tol = 1e-8, int max_cycles = 200,

@@ -151,6 +151,9 @@ int pmg_debug_chain_trace(int mode, unsigned long long* out, int cap);
 int pmg_debug_skew_trace(int mode, unsigned long long* out, int cap);
 /* the same for the rotating-lane sweeps: 4 u64 per warp block */
 int pmg_debug_wave_trace(int mode, unsigned long long* out, int cap);
+/* keep (mode 1) / drop (0) a copy of every rotating-lane sweep's output; mode 2 + kind (L 0, U 1,
+ * GS 2) copies the last one (v-space) into out; returns its length */
+int pmg_debug_wave_dump(int mode, double* out, int cap);
 
 #ifdef __cplusplus
 }

@@ -172,6 +172,71 @@ PmgHierarchy build_hierarchy(const HierarchyInputs& in, Smoother smoother, int n
     return H;
 }
 
+// ------------------------------------------------------------------ problem assembly (host)
+namespace {
+[[noreturn]] void host_fail(const char* what) {
+    throw std::runtime_error(std::string(what) + ": " + iga_last_error());
+}
+CsrMatrix host_csr(const iga_problem* h, int kind, int l) {
+    CsrMatrix M;
+    int64_t nnz = 0;
+    if (iga_problem_csr_shape(h, kind, l, &M.nrows, &M.ncols, &nnz)) host_fail("assemble");
+    M.row_offsets.resize(size_t(M.nrows) + 1);
+    M.col_indices.resize(size_t(nnz));
+    M.values.resize(size_t(nnz));
+    if (iga_problem_csr_copy(h, kind, l, M.row_offsets.data(), M.col_indices.data(), M.values.data()))
+        host_fail("assemble");
+    return M;
+}
+Vector host_vec(const iga_problem* h, int kind, int l) {
+    Vector v(size_t(iga_problem_vec_len(h, kind, l)));
+    if (iga_problem_vec_copy(h, kind, l, v.data())) host_fail("assemble");
+    return v;
+}
+}  // namespace
+
+ProblemSpec config_spec(int config, int degree) {
+    ProblemSpec s{};
+    if (iga_config_spec(config, degree, &s)) host_fail("config_spec");
+    return s;
+}
+
+Problem assemble(const ProblemSpec& spec) {
+    iga_problem* h = nullptr;
+    if (iga_problem_build(&spec, &h)) host_fail("assemble");
+    std::unique_ptr<iga_problem, void (*)(iga_problem*)> guard(h, iga_problem_free);
+    Problem pb;
+    const int np = iga_problem_num_plevels(h), nh = iga_problem_num_hlevels(h);
+    for (int l = 0; l < np; ++l) {
+        PLevelInput L;
+        L.degree = iga_problem_degree(h, l);
+        L.A = host_csr(h, IGA_MAT_A, l);
+        L.lumped_mass = host_vec(h, IGA_VEC_ML, l);
+        if (l + 1 < np) {
+            L.P = host_csr(h, IGA_MAT_P, l);
+            L.PT = host_csr(h, IGA_MAT_PT, l);
+        }
+        pb.inputs.plevels.push_back(std::move(L));
+    }
+    for (int j = 0; j < nh; ++j) {
+        HLevelInput L;
+        if (j > 0) L.A = host_csr(h, IGA_MAT_HA, j);
+        if (j + 1 < nh) {
+            L.P = host_csr(h, IGA_MAT_HP, j);
+            L.PT = host_csr(h, IGA_MAT_HPT, j);
+        }
+        pb.inputs.hlevels.push_back(std::move(L));
+    }
+    pb.f = host_vec(h, IGA_VEC_F, 0);
+    pb.u0 = host_vec(h, IGA_VEC_U0, 0);
+    return pb;
+}
+
+PmgHierarchy build_hierarchy(const ProblemSpec& spec, Smoother smoother, int nu1, int nu2, double tau,
+                             double fillfactor, Ordering ordering) {
+    return build_hierarchy(assemble(spec).inputs, smoother, nu1, nu2, tau, fillfactor, ordering);
+}
+
 double PmgHierarchy::setup_seconds() const {
     pmg_hier_stats s{};
     pmg_hier_get_stats(h_.get(), &s);
@@ -194,7 +259,7 @@ Vector prolongate(const PmgHierarchy& H, int level, const Vector& v) {
     return out;
 }
 
-Vector restrict_(const PmgHierarchy& H, int level, const Vector& r) {
+Vector restrict(const PmgHierarchy& H, int level, const Vector& r) {
     if (level < 0 || level + 1 >= int(H.sizes_.size())) throw std::invalid_argument("restrict: bad level");
     need(r.size(), size_t(H.sizes_[level]), "restrict");
     Vector out(H.sizes_[level + 1]);

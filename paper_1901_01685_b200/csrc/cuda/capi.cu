@@ -1474,6 +1474,21 @@ int pmg_debug_wave_trace(int mode, unsigned long long* out, int cap) {
     return g_wave_trace_n;
 }
 
+// diagnostics: mode 1/0 turns keeping a copy of every wave sweep's output on/off; mode 2+kind
+// copies the last output of that kind (0 L, 1 U, 2 GS; v-space) into out; returns its length
+int pmg_debug_wave_dump(int mode, double* out, int cap) {
+    if (mode == 0 || mode == 1) {
+        g_wave_dump = mode == 1;
+        return 0;
+    }
+    const int k = mode - 2;
+    if (k < 0 || k > 2 || !g_wave_dump_buf[k]) return 0;
+    const int n = std::min(g_wave_dump_n[k], cap);
+    if (cudaDeviceSynchronize() != cudaSuccess) return -1;
+    if (cudaMemcpy(out, g_wave_dump_buf[k], sizeof(double) * n, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+    return n;
+}
+
 // ms_by_class[0..6]: resid(A_p), L-solve(p), U-solve(p), GS(p), p-transfers, coarse (p<finest and
 // h-MG), misc; [7] = total launches, [8..14] = launches per class.  enable: n_classes < 0 turns
 // profiling on (-1) / off (-2) and resets the counters.

@@ -110,7 +110,6 @@ struct WaveArgs {
     const int32_t* hsl;
     const int64_t* off;
     int32_t n, seg, nseg, nblk, ntask, W, dm, ry;
-    unsigned sbase;  // shared-window address of the dynamic shared memory the items were built for
     unsigned long long* trace;  // diagnostics (null: off): per block [start, step 200, end, task]
     Layout lay;
     int* ticket;
@@ -134,6 +133,17 @@ __device__ __forceinline__ int ld_vol_s(unsigned a) {
     asm volatile("ld.volatile.shared.b32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
     return v;
 }
+// progress reads are acquire loads: on shared memory this is a plain LDS, but the compiler may
+// not move the ring loads that follow it above it (a relaxed read lets ptxas hoist them over the
+// spin loop, reading values before their producer published them)
+__device__ __forceinline__ int ld_acq_s(unsigned a) {
+    int v;
+    asm volatile("ld.acquire.cta.shared.b32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_rel_s(unsigned a, int v) {
+    asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
 __device__ __forceinline__ void st_vol_s(unsigned a, int v) {
     asm volatile("st.volatile.shared.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
@@ -142,7 +152,7 @@ __device__ __forceinline__ int wait_ge(unsigned addr, int pv, int need) {
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "L:\n\tsetp.ge.s32 p, %0, %2;\n\t@p bra.uni D;\n\t"
-        "ld.volatile.shared.b32 %0, [%1];\n\tbra.uni L;\n"
+        "ld.acquire.cta.shared.b32 %0, [%1];\n\tbra.uni L;\n"
         "D:\n\t}"
         : "+r"(pv)
         : "r"(addr), "r"(need)
@@ -197,7 +207,6 @@ __global__ void __launch_bounds__(32 * (WMAX + 2)) k_wave(WaveArgs a) {
     constexpr int DS = 4 - C;  // first used slot; U / GS chunk 0: 1/diagonal there
     extern __shared__ __align__(128) unsigned char wave_smem[];
     const unsigned sb = smem_u32(wave_smem);
-    if (sb != a.sbase) __trap();  // the items hold absolute shared-memory addresses
     const Layout& ly = a.lay;
     const int W = a.W, DM = a.dm, RY = a.ry, RYS = a.ry + 1;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -288,7 +297,7 @@ __global__ void __launch_bounds__(32 * (WMAX + 2)) k_wave(WaveArgs a) {
             for (;;) {
                 int pr[WMAX];
                 for (int w = 0; w < WMAX; ++w)  // a warp that finished its steps reads no ring cell
-                    pr[w] = w < W ? max(ld_vol_s(s_prog + 4 * w), ld_vol_s(sb + ly.rdp + 4 * w)) : INF;
+                    pr[w] = w < W ? max(ld_acq_s(s_prog + 4 * w), ld_acq_s(sb + ly.rdp + 4 * w)) : INF;
                 double v[MAXD];
 #pragma unroll
                 for (int d = 0; d < MAXD; ++d) {
@@ -312,7 +321,7 @@ __global__ void __launch_bounds__(32 * (WMAX + 2)) k_wave(WaveArgs a) {
                 }
                 __syncwarp();
                 if (vp > pub) {
-                    if (lane == 0) st_vol_s(s_vprog, vp);
+                    if (lane == 0) st_rel_s(s_vprog, vp);
                     pub = vp;
                 }
                 if (vp >= INF) break;
@@ -338,7 +347,7 @@ __global__ void __launch_bounds__(32 * (WMAX + 2)) k_wave(WaveArgs a) {
         const int phase = (P + D * k + rl) % NR;         // lane finalises at step t <=> t % NR == phase
         const int c0 = ((-1 - P - D * k) % NR + NR) % NR;  // finaliser of step t-1: gbase + ((t + c0) % NR)
         const unsigned pred = warp == 0 ? s_vprog : s_prog + 4 * (warp - 1);
-        const unsigned XB = sb + unsigned(ly.xb);
+        const unsigned XB = unsigned(ly.xb);
         const int myring = (DM + warp * SPW + k) * RYS;  // own ring (element index)
         const unsigned ibase = sb + ly.item + warp * PF * STEP_BYTES + lane * 16;
         const unsigned rbase = sb + ly.rhs + warp * NRH * G * SPW * 8 + k * 8;
@@ -362,20 +371,20 @@ __global__ void __launch_bounds__(32 * (WMAX + 2)) k_wave(WaveArgs a) {
             for (int j = 1; warp + j < W; ++j) {
                 const int need = (q + 1) * G + bpp[j];
                 if (need > -INF / 2)
-                    while (max(ld_vol_s(s_prog + 4 * (warp + j)), ld_vol_s(sb + ly.rdp + 4 * (warp + j))) < need) {
+                    while (max(ld_acq_s(s_prog + 4 * (warp + j)), ld_acq_s(sb + ly.rdp + 4 * (warp + j))) < need) {
                     }
             }
         };
         for (int q = 0; q < NG; ++q) refill(q);
         group_wait(0);
-        int pv = ld_vol_s(pred);
-        while (pv < Lw - 1) pv = ld_vol_s(pred);  // the prologue loads below belong to step -1
+        int pv = ld_acq_s(pred);
+        while (pv < Lw - 1) pv = ld_acq_s(pred);  // the prologue loads below belong to step -1
         Step cur, nxt, now;
         fetch_item(ibase, now);
         fetch_item(ibase + STEP_BYTES, cur);
         double yc[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) yc[q] = lds_f64(now.o[q]);
+        for (int q = 0; q < 4; ++q) yc[q] = lds_f64(sb + now.o[q]);
         double rh = lds_f64(rbase), sr = 0.0;
         if (K == kSkewGS) sr = lds_f64(sbase2);
         double acc = 0.0, x = 0.0;
@@ -396,13 +405,13 @@ __global__ void __launch_bounds__(32 * (WMAX + 2)) k_wave(WaveArgs a) {
                 // value is a valid lower bound); reloaded now for the next step's test, off the chain
                 if (u % CHK == 0) {  // one test covers the loads of steps t .. t+CHK-1
                     pv = wait_ge(pred, pv, t + CHK - 1 + Lw);
-                    pv = ld_vol_s(pred);
+                    pv = ld_acq_s(pred);
                 }
                 const double xb = __shfl_sync(FULL, x, gbase + ((u + c0) & (NR - 1)));
                 if (u == G - 2) group_wait(qg + 1);
                 double yn[4];
 #pragma unroll
-                for (int q = DS; q < 4; ++q) yn[q] = lds_f64(cur.o[q]);
+                for (int q = DS; q < 4; ++q) yn[q] = lds_f64(sb + cur.o[q]);
                 fetch_item(ibase + ((t + 2) % PF) * STEP_BYTES, nxt);
                 const int rs = ((t + 1) % (NRH * G)) * SPW * 8;
                 const double rhn = lds_f64(rbase + rs);
@@ -439,7 +448,7 @@ __global__ void __launch_bounds__(32 * (WMAX + 2)) k_wave(WaveArgs a) {
         // finished: no ring cell is read any more; "done" is published once the predecessor is
         // done (keeps the progress chain valid)
         st_vol_s(sb + ly.rdp + 4 * warp, INF);
-        while (ld_vol_s(pred) < INF) {
+        while (ld_acq_s(pred) < INF) {
         }
         st_vol_s(s_me, INF);
     }
@@ -555,8 +564,8 @@ __global__ void k_wave_req2(Sell S, const int32_t* nlow, int32_t seg, int NR, in
 template <int K>
 __global__ void k_wave_fill(Sell S, const int32_t* __restrict__ nlow, const double* __restrict__ dinv, int32_t seg,
                             int32_t nseg, const int32_t* __restrict__ Db, const int64_t* __restrict__ off, int32_t nblk,
-                            int NR, int C, int W, int DM, int RY, int ring0, int xb, unsigned sbase,
-                            int64_t nsteps, uint4* __restrict__ item) {
+                            int NR, int C, int W, int DM, int RY, int ring0, int xb, int64_t nsteps,
+                            uint4* __restrict__ item) {
     const int64_t gid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (gid >= nsteps * 32) return;
     const int64_t ts = gid >> 5;
@@ -576,7 +585,7 @@ __global__ void k_wave_fill(Sell S, const int32_t* __restrict__ nlow, const doub
     const int s = ((rl - base) % NR + NR) % NR;
     const int ix = base + s;           // the row this lane works on (chunk s)
     const int RYS = RY + 1;
-    const unsigned zero = sbase + ring0 + 8 * RY;
+    const unsigned zero = ring0 + 8 * RY;
     Step it;
     for (int q = 0; q < 4; ++q) {
         it.w[q] = 0.0;
@@ -594,11 +603,11 @@ __global__ void k_wave_fill(Sell S, const int32_t* __restrict__ nlow, const doub
             const int gc = c / seg, jx = c - gc * seg, d = g - gc;
             it.w[q] = r.val(i);
             if (d == 0 && q == 3 && jx == ix - s - 1) {
-                it.o[q] = sbase + unsigned(xb);
+                it.o[q] = unsigned(xb);
             } else {  // the cell of the step that finalised row jx of segment gc
                 const int ridx = DM + (gc - g0);
                 const int pstep = jx + P + Db[gc / SPW] * (gc % SPW);
-                it.o[q] = sbase + unsigned(ring0 + 8 * (ridx * RYS + (pstep & (RY - 1))));
+                it.o[q] = unsigned(ring0 + 8 * (ridx * RYS + (pstep & (RY - 1))));
             }
         }
     }
@@ -645,28 +654,6 @@ void launch_req(const Sell& S, const int32_t* nlow, int32_t seg, int NR, int C, 
     PMG_LAUNCH_CHECK();
 }
 
-__global__ void k_sbase(unsigned* out) {
-    extern __shared__ __align__(128) unsigned char probe_smem[];
-    *out = smem_u32(probe_smem);
-}
-
-// shared-window address of a kernel's dynamic shared memory (no static shared memory, no
-// cluster): the items are built with it, k_wave checks it
-unsigned dyn_smem_base(cudaStream_t st) {
-    static const unsigned base = [st] {
-        unsigned* d = nullptr;
-        unsigned h = 0;
-        PMG_CUDA(cudaMalloc(&d, sizeof(unsigned)));
-        k_sbase<<<1, 32, 128, st>>>(d);
-        PMG_LAUNCH_CHECK();
-        PMG_CUDA(cudaMemcpyAsync(&h, d, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
-        PMG_CUDA(cudaStreamSynchronize(st));
-        cudaFree(d);
-        return h;
-    }();
-    return base;
-}
-
 int smem_limit() {
     static const int lim = [] {
         int dev = 0, v = 0;
@@ -679,6 +666,9 @@ int smem_limit() {
 
 }  // namespace
 
+bool g_wave_dump = false;
+double* g_wave_dump_buf[3] = {nullptr, nullptr, nullptr};
+int g_wave_dump_n[3] = {0, 0, 0};
 bool g_wave_trace_on = false;
 unsigned long long* g_wave_trace = nullptr;
 int g_wave_trace_n = 0;
@@ -847,16 +837,15 @@ bool wave_plan(const Sell& S, const double* dinv, int32_t seg, SkewKind kind, in
     PMG_CUDA(cudaMemcpyAsync(hrd, hhr.data(), sizeof(int32_t) * hhr.size(), cudaMemcpyHostToDevice, st));
     PMG_CUDA(cudaMemcpyAsync(offd, hoff.data(), sizeof(int64_t) * (nblk + 1), cudaMemcpyHostToDevice, st));
     const int nf = ceil_div(nsteps * 32, 256);
-    const unsigned sbase = dyn_smem_base(st);
     if (kind == kSkewL)
         k_wave_fill<kSkewL><<<nf, 256, 0, st>>>(S, nlow, dinv, seg, nseg, p.Db, offd, nblk, NR, C, W, dm, ry, ly.ring,
-                                                ly.xb, sbase, nsteps, item);
+                                                ly.xb, nsteps, item);
     else if (kind == kSkewU)
         k_wave_fill<kSkewU><<<nf, 256, 0, st>>>(S, nlow, dinv, seg, nseg, p.Db, offd, nblk, NR, C, W, dm, ry, ly.ring,
-                                                ly.xb, sbase, nsteps, item);
+                                                ly.xb, nsteps, item);
     else
         k_wave_fill<kSkewGS><<<nf, 256, 0, st>>>(S, nlow, dinv, seg, nseg, p.Db, offd, nblk, NR, C, W, dm, ry,
-                                                 ly.ring, ly.xb, sbase, nsteps, item);
+                                                 ly.ring, ly.xb, nsteps, item);
     PMG_LAUNCH_CHECK();
     PMG_CUDA(cudaStreamSynchronize(st));
     cudaFree(p.R);
@@ -882,7 +871,6 @@ bool wave_plan(const Sell& S, const double* dinv, int32_t seg, SkewKind kind, in
     plan.hoff = hod;
     plan.hrb = hrd;
     plan.hsl = hsd;
-    plan.sbase = sbase;
     plan.off = offd;
     plan.item = item;
     plan.lead = sl.empty() ? hL[0] : sl[sl.size() / 2];
@@ -948,7 +936,6 @@ void wave_sweep(const WaveOp& op, int* ticket, cudaStream_t st) {
     a.hoff = p.hoff;
     a.hrb = p.hrb;
     a.hsl = p.hsl;
-    a.sbase = p.sbase;
     a.trace = nullptr;
     if (g_wave_trace_on) {  // one-shot trace of the next sweep (diagnostics)
         g_wave_trace_on = false;
@@ -974,6 +961,13 @@ void wave_sweep(const WaveOp& op, int* ticket, cudaStream_t st) {
     if (op.kind == kSkewL) launch_kind<kSkewL>(p, a, grid, st);
     else if (op.kind == kSkewU) launch_kind<kSkewU>(p, a, grid, st);
     else launch_kind<kSkewGS>(p, a, grid, st);
+    if (g_wave_dump) {  // diagnostics: keep a copy of this sweep's output (v-space), per kind
+        double*& d = g_wave_dump_buf[op.kind];
+        cudaFree(d);
+        PMG_CUDA(cudaMalloc(&d, sizeof(double) * n));
+        PMG_CUDA(cudaMemcpyAsync(d, op.out, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+        g_wave_dump_n[op.kind] = n;
+    }
     if (op.kind == kSkewU) {
         k_wave_upd<<<ceil_div(n, 256), 256, 0, st>>>(op.out, op.upd, n);
         PMG_LAUNCH_CHECK();

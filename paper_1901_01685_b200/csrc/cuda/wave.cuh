@@ -23,7 +23,6 @@ struct WavePlan {
     int32_t* hoff = nullptr;     // [ntask][8] bridge: halo row counts -> virtual progress of the previous block
     int32_t* hrb = nullptr;      // [ntask][w][8] bridge: halo row j may be written iff j < prog(w) + hrb
     int32_t* hsl = nullptr;      // [ntask][8] bridge: halo row j goes to ring cell (j + hsl) mod ry
-    unsigned sbase = 0;          // shared-window address of the kernel's dynamic shared memory
     int64_t* off = nullptr;      // [nblk+1] first step of each block in the item stream
     uint4* item = nullptr;       // [nsteps][3][32]
     int32_t lead = 0;            // median Lb (reporting)
@@ -54,6 +53,9 @@ void wave_sweep(const WaveOp& op, int* ticket, cudaStream_t st);
 // diagnostics: one-shot trace of the next sweep, 4 u64 per warp block
 // [globaltimer at step 0, at step 192, at the end, CTA task]
 extern bool g_wave_trace_on;
+extern bool g_wave_dump;              // keep a copy of each sweep's output (per kind)
+extern double* g_wave_dump_buf[3];
+extern int g_wave_dump_n[3];
 extern unsigned long long* g_wave_trace;
 extern int g_wave_trace_n;
 
