@@ -41,6 +41,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-bicgstab", action="store_true", help="skip the BiCGSTAB sub-measurement")
     ap.add_argument("--cpu-sample-cycles", type=int, default=0, help="0: a full oracle solve")
+    ap.add_argument("--cpu-single-thread", action="store_true", help="also time the oracle on one pinned core")
     return ap.parse_args()
 
 
@@ -153,6 +154,41 @@ def algorithmic_bytes(pb, H):
         nc = P.ncols
         out["transfer"] = (csr(PT) + 8 * n + 16 * nc) + (csr(P) + 8 * nc + 24 * n)  # restrict + prolong-add, per cycle
     return out
+
+
+def cycle_bytes(pb, H, facs):
+    """Algorithmic bytes of one V-cycle over EVERY level: the fine p-level
+    (3 residuals, 2 smoothing steps, restrict + prolong), coarser p-levels (config 3), and the p=1
+    h-multigrid correction (per h-level: 2 ILUT steps, 2 residuals, restrict, prolong-add);
+    CSR(X) = 12 nnz + 4 (rows+1), vectors counted once per kernel."""
+    csr = lambda M: 12 * M.nnz + 4 * (M.nrows + 1)
+    lsweep = lambda st, n: 12 * st["nnz_L"] + 4 * (n + 1) + 24 * n
+    usweep = lambda st, n: 12 * (st["nnz_U"] - n) + 4 * (n + 1) + 48 * n
+    ilut = H.smoother == "ilut"
+    fi = 0
+    total = 0
+    npl = len(pb.plevels)
+    for l, lev in enumerate(pb.plevels[:-1]):
+        n = lev.A.nrows
+        nres = 3 if l == 0 else 2
+        total += nres * (csr(lev.A) + 24 * n)
+        if ilut:
+            st = facs[fi]
+            fi += 1
+            total += 2 * (lsweep(st, n) + usweep(st, n))
+        else:
+            total += 2 * (csr(lev.A) + 32 * n)
+        nc = lev.P.ncols
+        total += (csr(lev.PT) + 8 * n + 16 * nc) + (csr(lev.P) + 8 * nc + 24 * n)
+    hmg = 0
+    for j, lev in enumerate(pb.hlevels[:-1]):
+        n = lev.A.nrows
+        st = facs[fi]
+        fi += 1
+        nc = lev.P.ncols
+        hmg += 2 * (lsweep(st, n) + usweep(st, n)) + 2 * (csr(lev.A) + 24 * n)
+        hmg += (csr(lev.PT) + 8 * n + 8 * nc) + (csr(lev.P) + 8 * nc + 16 * n)
+    return total + hmg, hmg
 
 
 def run_reference(args, ws, rank):
@@ -316,7 +352,7 @@ def main():
             "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_kind, "bytes_per_launch": bytes_dom,
             "ms_per_launch": per_launch_ms, "launches": launches_dom,
             "note": "triangular sweeps are bounded by their dependency depth (see 'triangular') and the per-segment "
-                    "lead of the skewed-warp wavefront, not by HBM"}
+                    "lead of the rotating-lane wavefront, not by HBM"}
     # the HBM-bound kernel of the cycle (residual SpMV), for kernel quality
     if la.get("resid_fine", 0) > 0:
         r_ms = ms["resid_fine"] / la["resid_fine"]
@@ -331,12 +367,9 @@ def main():
             gbs = ab[k2] / (ms_op * 1e-3) / 1e9
             per_kernel[k2] = {"ms": ms_op, "bytes": ab[k2], "achieved_GBs": gbs, "frac": gbs / peak}
     roof["per_kernel"] = per_kernel
-    # per-V-cycle aggregate fraction
-    total_bytes_cycle = ab["resid_fine"] * 3 + ab.get("transfer", 0)
-    if "lsolve_fine" in ab:
-        total_bytes_cycle += 2 * (ab["lsolve_fine"] + ab["usolve_fine"])
-    else:
-        total_bytes_cycle += 2 * ab["gs_fine"]
+    # per-V-cycle aggregate fraction: every level, the h-MG correction included
+    fstats = [dict(F.stats(), n=F.n) for F in H.factors()]
+    total_bytes_cycle, hmg_bytes = cycle_bytes(pb, H, fstats)
     ms_cycle = 1e3 * T_local / max(cycles, 1)
     breakdown = {k: {"ms_total": v, "launches": la.get(k, 0)} for k, v in ms.items()}
 
@@ -360,10 +393,12 @@ def main():
                 "ms_per_step": 1e3 * T_e2e / args.steps},
         "gpu_launches": kt_timed["launches"],
         "roofline": roof,
-        "v_cycle": {"ms": ms_cycle, "algorithmic_bytes": total_bytes_cycle,
+        "v_cycle": {"ms": ms_cycle, "algorithmic_bytes": total_bytes_cycle, "hmg_bytes": hmg_bytes,
                     "achieved_GBs": total_bytes_cycle / (ms_cycle * 1e-3) / 1e9,
-                    "frac": total_bytes_cycle / (ms_cycle * 1e-3) / 1e9 / peak},
+                    "frac": total_bytes_cycle / (ms_cycle * 1e-3) / 1e9 / peak,
+                    "note": "all levels, including the p=1 h-multigrid correction (hmg_bytes)"},
         "kernel_ms": breakdown,
+        "kernel_ms_note": "per-class device time of one extra (untimed) solve with CUDA events around every launch",
         "clocks": clk,
         "cpu_baseline": cpu,
         "bicgstab": bicg,
@@ -374,31 +409,35 @@ def main():
                               "rows_per_level_L": fs["rows_per_level_L"], "rows_per_level_U": fs["rows_per_level_U"],
                               "nnz_L": fs["nnz_L"], "nnz_U": fs["nnz_U"], "sweep_kernel": fs.get("sweep"),
                               "segment_rows": fs.get("segment"),
-                              "steps_per_segment_LU": list(fs.get("skew_D", ())),
-                              "note": "skewed-warp wavefront: one grid row per segment, consecutive segments "
-                                      "lag by steps_per_segment steps; the DAG depth per segment is "
-                                      "levels / (n / segment_rows)"}
+                              "lead_steps_LU": list(fs.get("skew_D", ())),
+                              "factors": [{"n": f["n"],
+                                           "levels_LU": [f["levels_L"], f["levels_U"]],
+                                           "rows_per_level_LU": [round(f["rows_per_level_L"], 2),
+                                                                 round(f["rows_per_level_U"], 2)],
+                                           "sweep": f["sweep"], "segment_rows": f["segment"],
+                                           "lead_steps_LU": list(f["skew_D"])} for f in fstats],
+                              "note": "rotating-lane wavefront (wave.cu): one grid row per segment, a warp block "
+                                      "of segments lags the previous block by lead_steps; factors = every "
+                                      "ILUT factor of the hierarchy (p-levels, then the p=1 h-levels)"}
     print(json.dumps(line), flush=True)
 
 
-NCU_KERNEL = {"lsolve_fine": "void unnamed>::k_chain<0>", "usolve_fine": "void unnamed>::k_chain<1>",
-              "gs_fine": "void unnamed>::k_chain<2>", "resid_fine": "void k_rowop<1, 1>"}
+NCU_KERNEL = {"lsolve_fine": "k_wave<0, 32, 4>", "usolve_fine": "k_wave<1, 32, 4>", "gs_fine": "k_wave<2, 16, 4>",
+              "resid_fine": "k_rowop<1, 1>"}
+TRAFFIC = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "round2", "traffic.json")
 
 
 def ncu_traffic(dom, args):
     """DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture
     (profiles/round1/traffic.json, made by scripts/profile_round1.sh on the default workload)."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "round1", "traffic.json")
-    if args.config != 5 or args.smoother != "ilut" or not os.path.exists(path):
+    if args.config != 5 or not os.path.exists(TRAFFIC):
         return None, None
-    tab = json.load(open(path))
-    rec = tab.get(NCU_KERNEL.get(dom, ""))
-    if not rec:  # skewed-warp sweeps: the template arguments carry the layout
-        pre = {"lsolve_fine": "k_skew<0", "usolve_fine": "k_skew<1"}.get(dom)
-        rec = next((v for k, v in tab.items() if pre and pre in k), None)
+    tab = json.load(open(TRAFFIC))
+    key = NCU_KERNEL.get(dom, "")
+    rec = next((v for k, v in tab.items() if key and key in k), None)
     if not rec:
         return None, None
-    return rec["dram_bytes_per_launch"], "profiles/round1/traffic.json (ncu --set full, config 5 ILUT)"
+    return rec["dram_bytes_per_launch"], "profiles/round2/traffic.json (ncu --set full, config 5)"
 
 
 def cpu_baseline(pb, H, args):
@@ -423,10 +462,26 @@ def cpu_baseline(pb, H, args):
         t0 = time.perf_counter()
         u, rep = Ho.solve(pb.f, pb.u0, max_cycles=max_c)
         wall = time.perf_counter() - t0
-        return {"value": pb.n * rep["cycles"] / rep["solve_seconds"], "unit": UNIT, "cores": cores, "kind": "port",
-                "sample": f"one oracle solve of the same system ({rep['cycles']} cycles, {wall:.1f}s wall; "
-                          f"row-parallel SpMV/transfers, sequential sweeps), ILUT factors imported from the GPU "
-                          f"(bit-identical to the oracle's, tests/test_gpu_parity.py)", "cycles": rep["cycles"]}
+        out = {"value": pb.n * rep["cycles"] / rep["solve_seconds"], "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": f"one oracle solve of the same system ({rep['cycles']} cycles, {wall:.1f}s wall; "
+                         f"row-parallel SpMV/transfers, sequential sweeps), ILUT factors imported from the GPU "
+                         f"(bit-identical to the oracle's, tests/test_gpu_parity.py)", "cycles": rep["cycles"]}
+        if args.cpu_single_thread:  # one pinned core, median of 3 (the paper's serial setting)
+            aff = os.sched_getaffinity(0)
+            try:
+                os.sched_setaffinity(0, {min(aff)})
+                O.set_threads(1)
+                ts = []
+                for _ in range(3):
+                    _, r1 = Ho.solve(pb.f, pb.u0, max_cycles=max_c)
+                    ts.append(r1["solve_seconds"])
+            finally:
+                os.sched_setaffinity(0, aff)
+                O.set_threads(cores)
+            med = sorted(ts)[1]
+            out["single_thread"] = {"value": pb.n * r1["cycles"] / med, "unit": UNIT, "cores": 1,
+                                    "seconds_median_of_3": med, "pinned_core": min(aff)}
+        return out
     except Exception as e:  # report, never hide
         return {"value": None, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "port", "sample": f"failed: {e}"}
 

@@ -109,6 +109,7 @@ struct WaveArgs {
     const int32_t* hrb;
     const int32_t* hsl;
     const int64_t* off;
+    unsigned sbase;  // shared-window address of the dynamic shared memory the items were built for
     int32_t n, seg, nseg, nblk, ntask, W, dm, ry;
     unsigned long long* trace;  // diagnostics (null: off): per block [start, step 200, end, task]
     Layout lay;
@@ -207,6 +208,7 @@ __global__ void __launch_bounds__(32 * (WMAX + 2)) k_wave(WaveArgs a) {
     constexpr int DS = 4 - C;  // first used slot; U / GS chunk 0: 1/diagonal there
     extern __shared__ __align__(128) unsigned char wave_smem[];
     const unsigned sb = smem_u32(wave_smem);
+    if (sb != a.sbase) __trap();  // the items hold absolute shared-memory addresses
     const Layout& ly = a.lay;
     const int W = a.W, DM = a.dm, RY = a.ry, RYS = a.ry + 1;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -347,7 +349,7 @@ __global__ void __launch_bounds__(32 * (WMAX + 2)) k_wave(WaveArgs a) {
         const int phase = (P + D * k + rl) % NR;         // lane finalises at step t <=> t % NR == phase
         const int c0 = ((-1 - P - D * k) % NR + NR) % NR;  // finaliser of step t-1: gbase + ((t + c0) % NR)
         const unsigned pred = warp == 0 ? s_vprog : s_prog + 4 * (warp - 1);
-        const unsigned XB = unsigned(ly.xb);
+        const unsigned XB = sb + unsigned(ly.xb);
         const int myring = (DM + warp * SPW + k) * RYS;  // own ring (element index)
         const unsigned ibase = sb + ly.item + warp * PF * STEP_BYTES + lane * 16;
         const unsigned rbase = sb + ly.rhs + warp * NRH * G * SPW * 8 + k * 8;
@@ -384,7 +386,7 @@ __global__ void __launch_bounds__(32 * (WMAX + 2)) k_wave(WaveArgs a) {
         fetch_item(ibase + STEP_BYTES, cur);
         double yc[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) yc[q] = lds_f64(sb + now.o[q]);
+        for (int q = 0; q < 4; ++q) yc[q] = lds_f64(now.o[q]);
         double rh = lds_f64(rbase), sr = 0.0;
         if (K == kSkewGS) sr = lds_f64(sbase2);
         double acc = 0.0, x = 0.0;
@@ -411,7 +413,7 @@ __global__ void __launch_bounds__(32 * (WMAX + 2)) k_wave(WaveArgs a) {
                 if (u == G - 2) group_wait(qg + 1);
                 double yn[4];
 #pragma unroll
-                for (int q = DS; q < 4; ++q) yn[q] = lds_f64(sb + cur.o[q]);
+                for (int q = DS; q < 4; ++q) yn[q] = lds_f64(cur.o[q]);
                 fetch_item(ibase + ((t + 2) % PF) * STEP_BYTES, nxt);
                 const int rs = ((t + 1) % (NRH * G)) * SPW * 8;
                 const double rhn = lds_f64(rbase + rs);
@@ -564,8 +566,8 @@ __global__ void k_wave_req2(Sell S, const int32_t* nlow, int32_t seg, int NR, in
 template <int K>
 __global__ void k_wave_fill(Sell S, const int32_t* __restrict__ nlow, const double* __restrict__ dinv, int32_t seg,
                             int32_t nseg, const int32_t* __restrict__ Db, const int64_t* __restrict__ off, int32_t nblk,
-                            int NR, int C, int W, int DM, int RY, int ring0, int xb, int64_t nsteps,
-                            uint4* __restrict__ item) {
+                            int NR, int C, int W, int DM, int RY, int ring0, int xb, unsigned sbase,
+                            int64_t nsteps, uint4* __restrict__ item) {
     const int64_t gid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (gid >= nsteps * 32) return;
     const int64_t ts = gid >> 5;
@@ -585,7 +587,7 @@ __global__ void k_wave_fill(Sell S, const int32_t* __restrict__ nlow, const doub
     const int s = ((rl - base) % NR + NR) % NR;
     const int ix = base + s;           // the row this lane works on (chunk s)
     const int RYS = RY + 1;
-    const unsigned zero = ring0 + 8 * RY;
+    const unsigned zero = sbase + ring0 + 8 * RY;
     Step it;
     for (int q = 0; q < 4; ++q) {
         it.w[q] = 0.0;
@@ -603,11 +605,11 @@ __global__ void k_wave_fill(Sell S, const int32_t* __restrict__ nlow, const doub
             const int gc = c / seg, jx = c - gc * seg, d = g - gc;
             it.w[q] = r.val(i);
             if (d == 0 && q == 3 && jx == ix - s - 1) {
-                it.o[q] = unsigned(xb);
+                it.o[q] = sbase + unsigned(xb);
             } else {  // the cell of the step that finalised row jx of segment gc
                 const int ridx = DM + (gc - g0);
                 const int pstep = jx + P + Db[gc / SPW] * (gc % SPW);
-                it.o[q] = unsigned(ring0 + 8 * (ridx * RYS + (pstep & (RY - 1))));
+                it.o[q] = sbase + unsigned(ring0 + 8 * (ridx * RYS + (pstep & (RY - 1))));
             }
         }
     }
@@ -652,6 +654,28 @@ void launch_req(const Sell& S, const int32_t* nlow, int32_t seg, int NR, int C, 
     if (second) k_wave_req2<K><<<nb, 256, 0, st>>>(S, nlow, seg, NR, C, p);
     else k_wave_req<K><<<nb, 256, 0, st>>>(S, nlow, seg, NR, C, p);
     PMG_LAUNCH_CHECK();
+}
+
+__global__ void k_sbase(unsigned* out) {
+    extern __shared__ __align__(128) unsigned char probe_smem[];
+    *out = smem_u32(probe_smem);
+}
+
+// shared-window address of a kernel's dynamic shared memory (no static shared memory, no
+// cluster): the items are built with it (absolute LDS addresses), k_wave checks it
+unsigned dyn_smem_base(cudaStream_t st) {
+    static const unsigned base = [st] {
+        unsigned* d = nullptr;
+        unsigned h = 0;
+        PMG_CUDA(cudaMalloc(&d, sizeof(unsigned)));
+        k_sbase<<<1, 32, 128, st>>>(d);
+        PMG_LAUNCH_CHECK();
+        PMG_CUDA(cudaMemcpyAsync(&h, d, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+        PMG_CUDA(cudaStreamSynchronize(st));
+        cudaFree(d);
+        return h;
+    }();
+    return base;
 }
 
 int smem_limit() {
@@ -837,15 +861,16 @@ bool wave_plan(const Sell& S, const double* dinv, int32_t seg, SkewKind kind, in
     PMG_CUDA(cudaMemcpyAsync(hrd, hhr.data(), sizeof(int32_t) * hhr.size(), cudaMemcpyHostToDevice, st));
     PMG_CUDA(cudaMemcpyAsync(offd, hoff.data(), sizeof(int64_t) * (nblk + 1), cudaMemcpyHostToDevice, st));
     const int nf = ceil_div(nsteps * 32, 256);
+    const unsigned sbase = dyn_smem_base(st);
     if (kind == kSkewL)
         k_wave_fill<kSkewL><<<nf, 256, 0, st>>>(S, nlow, dinv, seg, nseg, p.Db, offd, nblk, NR, C, W, dm, ry, ly.ring,
-                                                ly.xb, nsteps, item);
+                                                ly.xb, sbase, nsteps, item);
     else if (kind == kSkewU)
         k_wave_fill<kSkewU><<<nf, 256, 0, st>>>(S, nlow, dinv, seg, nseg, p.Db, offd, nblk, NR, C, W, dm, ry, ly.ring,
-                                                ly.xb, nsteps, item);
+                                                ly.xb, sbase, nsteps, item);
     else
         k_wave_fill<kSkewGS><<<nf, 256, 0, st>>>(S, nlow, dinv, seg, nseg, p.Db, offd, nblk, NR, C, W, dm, ry,
-                                                 ly.ring, ly.xb, nsteps, item);
+                                                 ly.ring, ly.xb, sbase, nsteps, item);
     PMG_LAUNCH_CHECK();
     PMG_CUDA(cudaStreamSynchronize(st));
     cudaFree(p.R);
@@ -871,6 +896,7 @@ bool wave_plan(const Sell& S, const double* dinv, int32_t seg, SkewKind kind, in
     plan.hoff = hod;
     plan.hrb = hrd;
     plan.hsl = hsd;
+    plan.sbase = sbase;
     plan.off = offd;
     plan.item = item;
     plan.lead = sl.empty() ? hL[0] : sl[sl.size() / 2];
@@ -936,6 +962,7 @@ void wave_sweep(const WaveOp& op, int* ticket, cudaStream_t st) {
     a.hoff = p.hoff;
     a.hrb = p.hrb;
     a.hsl = p.hsl;
+    a.sbase = p.sbase;
     a.trace = nullptr;
     if (g_wave_trace_on) {  // one-shot trace of the next sweep (diagnostics)
         g_wave_trace_on = false;

@@ -23,6 +23,7 @@ struct WavePlan {
     int32_t* hoff = nullptr;     // [ntask][8] bridge: halo row counts -> virtual progress of the previous block
     int32_t* hrb = nullptr;      // [ntask][w][8] bridge: halo row j may be written iff j < prog(w) + hrb
     int32_t* hsl = nullptr;      // [ntask][8] bridge: halo row j goes to ring cell (j + hsl) mod ry
+    unsigned sbase = 0;          // shared-window address of the kernel's dynamic shared memory
     int64_t* off = nullptr;      // [nblk+1] first step of each block in the item stream
     uint4* item = nullptr;       // [nsteps][3][32]
     int32_t lead = 0;            // median Lb (reporting)
