@@ -111,6 +111,7 @@ struct WaveArgs {
     const int64_t* off;
     unsigned sbase;  // shared-window address of the dynamic shared memory the items were built for
     int32_t n, seg, nseg, nblk, ntask, W, dm, ry;
+    int32_t slack;   // extra steps of lead over the plan's L_b (see wave_sweep)
     unsigned long long* trace;  // diagnostics (null: off): per block [start, step 200, end, task]
     Layout lay;
     int* ticket;
@@ -339,7 +340,7 @@ __global__ void __launch_bounds__(32 * (WMAX + 2)) k_wave(WaveArgs a) {
             st_vol_s(s_me, INF);
             continue;
         }
-        const int D = a.Db[b], Lw = a.Lb[b];
+        const int D = a.Db[b], Lw = a.Lb[b] + a.slack;
         const int NS = int(a.off[b + 1] - a.off[b]);
         const int nq = NS / G;
         const int k = lane / NR, rl = lane % NR, gbase = k * NR;
@@ -416,10 +417,19 @@ __global__ void __launch_bounds__(32 * (WMAX + 2)) k_wave(WaveArgs a) {
                 for (int q = DS; q < 4; ++q) yn[q] = lds_f64(cur.o[q]);
                 fetch_item(ibase + ((t + 2) % PF) * STEP_BYTES, nxt);
                 const int rs = ((t + 1) % (NRH * G)) * SPW * 8;
+#ifdef PMG_DIAG_NO_RHS
+                const double rhn = 1.0;
+                (void)rs;
+#else
                 const double rhn = lds_f64(rbase + rs);
+#endif
                 double srn = 0.0;
                 if (K == kSkewGS) srn = lds_f64(sbase2 + rs);
+#ifdef PMG_DIAG_NO_XBSEL
+                const double y3 = xb;
+#else
                 const double y3 = now.o[3] == XB ? xb : yc[3];
+#endif
                 double r = acc;
                 if (C == 4) r = r + now.w[0] * yc[0];
                 r = r + now.w[1] * yc[1];
@@ -431,8 +441,14 @@ __global__ void __launch_bounds__(32 * (WMAX + 2)) k_wave(WaveArgs a) {
                 // ring cells are indexed by the step that finalised the value (cells of
                 // rows outside the segment are never read); the output only for real rows
                 if (stage0) rings[rgb + u] = x;
+#ifndef PMG_DIAG_NO_STG
                 if (stage0 && ix >= 0 && ix < rows) outp[ix] = x;
+#endif
+#ifdef PMG_DIAG_NO_RESET
+                acc = r;
+#else
                 acc = stage0 ? 0.0 : r;
+#endif
                 if (u % CHK == CHK - 1) st_vol_s(s_me, t + 1);
 #pragma unroll
                 for (int q = 0; q < 4; ++q) yc[q] = yn[q];
@@ -777,7 +793,7 @@ bool wave_plan(const Sell& S, const double* dinv, int32_t seg, SkewKind kind, in
             if (Wv > INT_MIN) need = std::max<int64_t>(need, chain + Wv);
         }
     }
-    need += 2 * G;
+    need += 2 * G + EMAX * 8;  // room for the run-time slack (wave_sweep) of up to 8 steps per block
     int ry = 64;
     while (ry < need) ry *= 2;
     // warps per CTA: as many as shared memory holds
@@ -963,6 +979,11 @@ void wave_sweep(const WaveOp& op, int* ticket, cudaStream_t st) {
     a.hrb = p.hrb;
     a.hsl = p.hsl;
     a.sbase = p.sbase;
+    // a consumer tests its predecessor's progress with a value read a step earlier; running
+    // `slack` steps further behind than the dependencies require lets that stale value pass, so
+    // a gated block steps at the free-running rate instead of spinning on every test
+    static const int slack = std::max(0, env_int("PMG_WAVE_SLACK", 0));
+    a.slack = slack;
     a.trace = nullptr;
     if (g_wave_trace_on) {  // one-shot trace of the next sweep (diagnostics)
         g_wave_trace_on = false;
