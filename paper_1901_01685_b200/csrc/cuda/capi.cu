@@ -118,6 +118,7 @@ struct pmg_csr_s {
     double* gs_diag = nullptr;
     int32_t* gs_nlow = nullptr;
     int32_t seg = 0;              // chained-segment length (0: level-scheduled sweeps)
+    std::vector<int32_t> starts;  // grid-row segments of the natural order (empty: no structure)
     int32_t* gs_split = nullptr;
     int32_t gs_gap = 0;
     bool gs_chain = false;        // chained GS sweep (else level-scheduled)
@@ -151,6 +152,7 @@ struct pmg_factor_s {
     int32_t max_row_L = 0, max_row_U = 0;
     double seconds = 0;
     int32_t seg = 0;                  // chained-segment length (0: level-scheduled sweeps)
+    std::vector<int32_t> starts;      // grid-row segments (rotating-lane sweeps)
     int32_t* rev = nullptr;           // v -> row for the U sweep (descending rows)
     int32_t *splitL = nullptr, *splitU = nullptr;
     bool skew = false;                // skewed-warp sweeps (short rows, short reach)
@@ -228,6 +230,7 @@ pmg_csr_s* make_csr(const pmg_csr_view& v, cudaStream_t st) {
     h->h_val.assign(v.val, v.val + h->A.nnz);
     h->band = pmg_host::bandwidth(v.nrows, v.rowptr, v.col);
     h->seg = force_levelsched() ? 0 : detect_segment(v.nrows, v.rowptr, v.col);
+    if (!force_levelsched() && v.nrows == v.ncols) h->starts = detect_segment_starts(v.nrows, v.rowptr, v.col);
     sell_build(h->S, v.nrows, h->A.rowptr, h->A.col, h->A.val, nullptr, kPickAll, nullptr, nullptr, st);
     PMG_CUDA(cudaStreamSynchronize(st));
     return h.release();
@@ -239,23 +242,15 @@ void ensure_gs(pmg_csr_s* h, cudaStream_t st) {
     level_sets(h->gs_lv, n, h->A.rowptr, h->A.col, kDepLower, st);
     h->gs_diag = dalloc<double>(n);
     h->gs_nlow = dalloc<int32_t>(n);
-    sell_build(h->gs, n, h->A.rowptr, h->A.col, h->A.val, h->seg > 0 ? nullptr : h->gs_lv.order, kPickOffDiag,
-               h->gs_diag, h->gs_nlow, st);
-    h->gs_chain = h->seg > 0;
-    if (h->gs_chain) {
-        h->gs_split = dalloc<int32_t>(n);
-        chain_split(h->gs, h->gs_nlow, h->seg, kChainGS, h->gs_split, st);
-        const ChainPlan pl = chain_plan(h->gs, h->gs_nlow, h->gs_split, h->seg, kChainGS, st);
-        h->gs_gap = pl.gap;
-        if (!pl.ok) {  // rows exceed the chain kernel's on-chip buffers: level-scheduled sweep
-            h->gs_chain = false;
-            sell_free(h->gs);
-            cudaFree(h->gs_split);
-            h->gs_split = nullptr;
-            sell_build(h->gs, n, h->A.rowptr, h->A.col, h->A.val, h->gs_lv.order, kPickOffDiag, h->gs_diag,
-                       h->gs_nlow, st);
-        }
-    }
+    // sliced layout in row order for the wavefront kernels (grid-row segments), level order for
+    // the level-scheduled fallback
+    bool natural = h->seg > 0 || !h->starts.empty();
+    auto build = [&](bool nat) {
+        sell_free(h->gs);
+        sell_build(h->gs, n, h->A.rowptr, h->A.col, h->A.val, nat ? nullptr : h->gs_lv.order, kPickOffDiag,
+                   h->gs_diag, h->gs_nlow, st);
+    };
+    build(natural);
     // first row (in row order) with a zero or missing diagonal -> SPEC.md:237 smoother error
     std::vector<double> dg(n);
     std::vector<int32_t> ord(n);
@@ -264,21 +259,42 @@ void ensure_gs(pmg_csr_s* h, cudaStream_t st) {
     PMG_CUDA(cudaStreamSynchronize(st));
     int64_t zr = -1;
     for (int32_t p = 0; p < n; ++p) {
-        const int32_t row = h->gs_chain ? p : ord[p];
+        const int32_t row = natural ? p : ord[p];
         if (dg[p] == 0.0 && (zr < 0 || row < zr)) zr = row;
     }
     h->gs_zero_row = zr;
     reciprocal_inplace(h->gs_diag, n, st);
-    const char* sk = getenv("PMG_SKEW");
-    if (h->gs_chain && !(sk && sk[0] == '0')) {  // skewed-warp GS sweeps over the lower entries
+    int32_t mx = 0;  // longest lower part
+    if (natural) {
         std::vector<int32_t> nl(n);
         PMG_CUDA(cudaMemcpyAsync(nl.data(), h->gs_nlow, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
         PMG_CUDA(cudaStreamSynchronize(st));
-        int32_t mx = 0;
         for (int32_t v : nl) mx = std::max(mx, v);
-        const char* wv = getenv("PMG_WAVE");
-        if (!(wv && wv[0] == '0')) h->gs_wave = wave_plan(h->gs, h->gs_diag, h->seg, kSkewGS, mx, h->gs_wplan, st, h->gs_nlow);
-        if (!h->gs_wave) h->gs_skew = skew_plan(h->gs, h->gs_diag, h->seg, kSkewGS, mx, h->gs_plan, st, h->gs_nlow);
+    }
+    // 1. rotating-lane GS sweep over the lower entries (any grid-row segments)
+    const char* wv = getenv("PMG_WAVE");
+    if (!h->starts.empty() && !(wv && wv[0] == '0'))
+        h->gs_wave = wave_plan(h->gs, h->gs_diag, h->starts, kSkewGS, mx, h->gs_wplan, st, h->gs_nlow);
+    // 2. uniform segments: chained GS, skewed warps where they fit
+    h->gs_chain = !h->gs_wave && h->seg > 0;
+    if (h->gs_chain) {
+        h->gs_split = dalloc<int32_t>(n);
+        chain_split(h->gs, h->gs_nlow, h->seg, kChainGS, h->gs_split, st);
+        const ChainPlan pl = chain_plan(h->gs, h->gs_nlow, h->gs_split, h->seg, kChainGS, st);
+        h->gs_gap = pl.gap;
+        if (!pl.ok) {  // rows exceed the chain kernel's on-chip buffers
+            h->gs_chain = false;
+            cudaFree(h->gs_split);
+            h->gs_split = nullptr;
+        }
+    }
+    const char* sk = getenv("PMG_SKEW");
+    if (h->gs_chain && !(sk && sk[0] == '0'))
+        h->gs_skew = skew_plan(h->gs, h->gs_diag, h->seg, kSkewGS, mx, h->gs_plan, st, h->gs_nlow);
+    // 3. level-scheduled sweep (level-order layout; the diagonal follows the layout)
+    if (!h->gs_wave && !h->gs_chain && natural) {
+        build(false);
+        reciprocal_inplace(h->gs_diag, n, st);
     }
     h->gs_ready = true;
 }
@@ -295,6 +311,7 @@ int make_factor(pmg_csr_s* A, double tau, double fillfactor, int ordering, pmg_f
     DevCsr owned;
     int32_t band = A->band;
     F->seg = A->seg;
+    F->starts = A->starts;
     if (ordering == PMG_ORDER_RCM) {
         F->h_perm = pmg_host::rcm_ordering(n, A->h_rowptr.data(), A->h_col.data());
         std::vector<int32_t> brp, bci;
@@ -317,42 +334,28 @@ int make_factor(pmg_csr_s* A, double tau, double fillfactor, int ordering, pmg_f
     level_sets(F->lvL, n, F->L.rowptr, F->L.col, kDepLower, st);
     level_sets(F->lvU, n, F->U.rowptr, F->U.col, kDepUpper, st);
     F->Udiag = dalloc<double>(n);
-    bool chain = F->seg > 0;
-    if (chain) {  // chained-segment layouts: L in row order, U in descending row order
-        F->rev = dalloc<int32_t>(n);
-        std::vector<int32_t> rv(n);
-        for (int32_t v = 0; v < n; ++v) rv[v] = n - 1 - v;
-        PMG_CUDA(cudaMemcpyAsync(F->rev, rv.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, st));
-        sell_build(F->Ls, n, F->L.rowptr, F->L.col, F->L.val, nullptr, kPickAll, nullptr, nullptr, st);
-        sell_build(F->Us, n, F->U.rowptr, F->U.col, F->U.val, F->rev, kPickOffDiagDesc, F->Udiag, nullptr, st);
-        F->splitL = dalloc<int32_t>(n);
-        F->splitU = dalloc<int32_t>(n);
-        chain_split(F->Ls, nullptr, F->seg, kChainL, F->splitL, st);
-        chain_split(F->Us, nullptr, F->seg, kChainU, F->splitU, st);
-        const ChainPlan pl = chain_plan(F->Ls, nullptr, F->splitL, F->seg, kChainL, st);
-        const ChainPlan pu = chain_plan(F->Us, nullptr, F->splitU, F->seg, kChainU, st);
-        F->gapL = pl.gap;
-        F->gapU = pu.gap;
-        if (getenv("PMG_VERBOSE"))
-            fprintf(stderr, "[pmg] factor n=%d seg=%d gap %d/%d in-seg %d/%d back %d/%d\n", F->n, F->seg, pl.gap,
-                    pu.gap, pl.max_in, pu.max_in, pl.max_back, pu.max_back);
-        if (!(pl.ok && pu.ok)) {  // rows exceed the chain kernel's on-chip buffers: level-scheduled sweeps
-            chain = false;
-            F->seg = 0;
-            sell_free(F->Ls);
-            sell_free(F->Us);
-            cudaFree(F->rev);
-            cudaFree(F->splitL);
-            cudaFree(F->splitU);
-            F->rev = F->splitL = F->splitU = nullptr;
+    // sliced layouts: natural order (L ascending, U descending rows) for the wavefront kernels,
+    // level order for the level-scheduled fallback
+    auto build_sells = [&](bool natural) {
+        sell_free(F->Ls);
+        sell_free(F->Us);
+        if (natural && !F->rev) {
+            F->rev = dalloc<int32_t>(n);
+            std::vector<int32_t> rv(n);
+            for (int32_t v = 0; v < n; ++v) rv[v] = n - 1 - v;
+            PMG_CUDA(cudaMemcpyAsync(F->rev, rv.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, st));
         }
-    }
-    if (!chain) {
-        sell_build(F->Ls, n, F->L.rowptr, F->L.col, F->L.val, F->lvL.order, kPickAll, nullptr, nullptr, st);
-        sell_build(F->Us, n, F->U.rowptr, F->U.col, F->U.val, F->lvU.order, kPickOffDiagDesc, F->Udiag, nullptr, st);
-    }
-    reciprocal_inplace(F->Udiag, n, st);  // nonzero: a zero pivot was reported above
-    // longest rows (reporting)
+        sell_build(F->Ls, n, F->L.rowptr, F->L.col, F->L.val, natural ? nullptr : F->lvL.order, kPickAll, nullptr,
+                   nullptr, st);
+        sell_build(F->Us, n, F->U.rowptr, F->U.col, F->U.val, natural ? F->rev : F->lvU.order, kPickOffDiagDesc,
+                   F->Udiag, nullptr, st);
+        reciprocal_inplace(F->Udiag, n, st);  // nonzero: a zero pivot was reported above
+    };
+    // wavefront kernels need the natural (unpermuted) order and grid-row segments
+    if (F->perm || force_levelsched()) F->starts.clear();
+    const bool natural = F->seg > 0 || !F->starts.empty();
+    build_sells(natural);
+    // longest rows (reporting, layouts)
     std::vector<int32_t> lr(n + 1), ur(n + 1);
     PMG_CUDA(cudaMemcpyAsync(lr.data(), F->L.rowptr, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToHost, st));
     PMG_CUDA(cudaMemcpyAsync(ur.data(), F->U.rowptr, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToHost, st));
@@ -364,20 +367,41 @@ int make_factor(pmg_csr_s* A, double tau, double fillfactor, int ordering, pmg_f
     // short rows (p=1 factors): the per-segment lag is dominated by the finisher batch
     F->bs = std::max(F->max_row_L, F->max_row_U) <= 16 ? 8 : 32;
     if (const char* e = getenv("PMG_CHAIN_BS")) F->bs = atoi(e);
-    // tensor-grid orderings: skewed-warp sweeps (skew.cu); PMG_SKEW=0 keeps the
-    // chained-segment kernel for every factor
+    // 1. rotating-lane sweeps (wave.cu) for every grid-row ordering, any segment lengths
     const char* sk = getenv("PMG_SKEW");
     const char* wv = getenv("PMG_WAVE");
-    if (F->seg > 0 && !F->perm && !(wv && wv[0] == '0')) {
-        const bool okL = wave_plan(F->Ls, nullptr, F->seg, kSkewL, F->max_row_L, F->waveL, st);
-        const bool okU = okL && wave_plan(F->Us, F->Udiag, F->seg, kSkewU, F->max_row_U - 1, F->waveU, st);
+    if (!F->starts.empty() && !(wv && wv[0] == '0')) {
+        const bool okL = wave_plan(F->Ls, nullptr, F->starts, kSkewL, F->max_row_L, F->waveL, st);
+        const bool okU =
+            okL && wave_plan(F->Us, F->Udiag, reversed_starts(F->starts), kSkewU, F->max_row_U - 1, F->waveU, st);
         F->wave = okL && okU;
         if (!F->wave) {
             wave_plan_free(F->waveL);
             wave_plan_free(F->waveU);
         }
     }
-    if (!F->wave && F->seg > 0 && !F->perm && !(sk && sk[0] == '0')) {
+    // 2. uniform segments: chained-segment sweeps, skewed warps where they fit
+    bool chain = !F->wave && F->seg > 0;
+    if (chain) {
+        F->splitL = dalloc<int32_t>(n);
+        F->splitU = dalloc<int32_t>(n);
+        chain_split(F->Ls, nullptr, F->seg, kChainL, F->splitL, st);
+        chain_split(F->Us, nullptr, F->seg, kChainU, F->splitU, st);
+        const ChainPlan pl = chain_plan(F->Ls, nullptr, F->splitL, F->seg, kChainL, st);
+        const ChainPlan pu = chain_plan(F->Us, nullptr, F->splitU, F->seg, kChainU, st);
+        F->gapL = pl.gap;
+        F->gapU = pu.gap;
+        if (getenv("PMG_VERBOSE"))
+            fprintf(stderr, "[pmg] factor n=%d seg=%d gap %d/%d in-seg %d/%d back %d/%d\n", F->n, F->seg, pl.gap,
+                    pu.gap, pl.max_in, pu.max_in, pl.max_back, pu.max_back);
+        if (!(pl.ok && pu.ok)) {  // rows exceed the chain kernel's on-chip buffers
+            chain = false;
+            cudaFree(F->splitL);
+            cudaFree(F->splitU);
+            F->splitL = F->splitU = nullptr;
+        }
+    }
+    if (chain && !F->perm && !(sk && sk[0] == '0')) {
         const bool okL = skew_plan(F->Ls, nullptr, F->seg, kSkewL, F->max_row_L, F->planL, st);
         const bool okU = okL && skew_plan(F->Us, F->Udiag, F->seg, kSkewU, F->max_row_U - 1, F->planU, st);
         F->skew = okL && okU;
@@ -389,6 +413,11 @@ int make_factor(pmg_csr_s* A, double tau, double fillfactor, int ordering, pmg_f
             fprintf(stderr, "[pmg] factor n=%d skew %d NRxC %dx%d D %d/%d dm %d/%d ring %d/%d\n", F->n, int(F->skew),
                     F->planL.nr, F->planL.c, F->planL.D, F->planU.D, F->planL.dm, F->planU.dm, F->planL.ry,
                     F->planU.ry);
+    }
+    // 3. level-scheduled sweeps (level-order layouts)
+    if (!F->wave && !chain) {
+        F->seg = 0;
+        if (natural) build_sells(false);
     }
     *out = F.release();
     return PMG_OK;

@@ -18,6 +18,7 @@
 // once per segment row-lag instead of once per level (47k levels for the config-5 L factor).
 #include <climits>
 #include <cstdlib>
+#include <algorithm>
 #include <vector>
 
 #include "chain.cuh"
@@ -666,6 +667,23 @@ void chain_sweep(const ChainOp& op, int* ticket, cudaStream_t st) {
         PMG_LAUNCH_CHECK();
     }
     if (spill) PMG_CUDA(cudaFreeAsync(spill, st));
+}
+
+// Grid-row segments of a natural ordering, any lengths: row r starts a segment when it does not
+// couple to row r-1 (the last DOF of the previous grid row sits at the far end of that row).
+// Empty when the pattern has no such structure (segments shorter than 8 rows on average).
+std::vector<int32_t> detect_segment_starts(int32_t n, const int32_t* rp, const int32_t* col) {
+    std::vector<int32_t> starts;
+    if (n < 64) return starts;
+    starts.push_back(0);
+    for (int32_t r = 1; r < n; ++r) {
+        const int32_t* b = col + rp[r];
+        const int32_t* e = col + rp[r + 1];
+        if (!std::binary_search(b, e, r - 1)) starts.push_back(r);
+    }
+    starts.push_back(n);
+    if (int64_t(starts.size() - 1) * 8 > n) starts.clear();
+    return starts;
 }
 
 int32_t detect_segment(int32_t n, const int32_t* rp, const int32_t* col) {

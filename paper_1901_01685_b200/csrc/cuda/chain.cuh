@@ -1,6 +1,8 @@
 // Chained-segment wavefront sweeps (L solve, U solve + update, Gauss-Seidel).
 #pragma once
 
+#include <vector>
+
 #include "sell.cuh"
 
 namespace pmg {
@@ -55,5 +57,6 @@ void chain_sweep(const ChainOp& op, int* ticket, cudaStream_t st);
 // grid-row length of a tensor-product natural ordering detected from the sparsity pattern of
 // the middle row (distance between the starts of consecutive column runs); 0 if none found
 int32_t detect_segment(int32_t n, const int32_t* h_rowptr, const int32_t* h_col);
+std::vector<int32_t> detect_segment_starts(int32_t n, const int32_t* h_rowptr, const int32_t* h_col);
 
 }  // namespace pmg

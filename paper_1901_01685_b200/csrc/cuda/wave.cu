@@ -98,6 +98,7 @@ Layout layout(int W, int SPW, int DM, int RY, bool gs) {
 }
 
 struct WaveArgs {
+    const int32_t* starts;  // [nseg+1] first v-row of every segment (grid row)
     const uint4* item;
     const double* rhs;
     const double* su;
@@ -213,7 +214,8 @@ __global__ void __launch_bounds__(32 * (WMAX + 2)) k_wave(WaveArgs a) {
     const Layout& ly = a.lay;
     const int W = a.W, DM = a.dm, RY = a.ry, RYS = a.ry + 1;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int n = a.n, S = a.seg;
+    const int n = a.n;
+    const int32_t* starts = a.starts;
     const unsigned s_prog = sb + ly.prog, s_vprog = sb + ly.vprog;
     int* task_p = reinterpret_cast<int*>(wave_smem + ly.task);
     double* rings = reinterpret_cast<double*>(wave_smem + ly.ring);
@@ -263,8 +265,10 @@ __global__ void __launch_bounds__(32 * (WMAX + 2)) k_wave(WaveArgs a) {
                         const int e = i * 32 + lane;
                         const int st = q * G + e / SPW, kk = e % SPW;
                         const int gg = (b0 + w) * SPW + kk, ix = st - P - Dw[w] * kk;
-                        const int64_t vv = int64_t(gg) * S + ix;
-                        const bool in = e < G * SPW && gg < a.nseg && ix >= 0 && ix < S && vv < n;
+                        const bool real = e < G * SPW && gg < a.nseg;
+                        const int s0 = real ? starts[gg] : 0, s1 = real ? starts[gg + 1] : 0;
+                        const int64_t vv = int64_t(s0) + ix;
+                        const bool in = real && ix >= 0 && ix < s1 - s0;
                         v[i] = in ? a.rhs[K == kSkewU ? int64_t(n) - 1 - vv : vv] : 0.0;
                         if (K == kSkewGS) s2[i] = in ? a.su[vv] : 0.0;
                     }
@@ -286,13 +290,14 @@ __global__ void __launch_bounds__(32 * (WMAX + 2)) k_wave(WaveArgs a) {
         if (warp == W + 1) {
             // ------------------------------------------------------------ bridge
             // halo segment g0-1-d (d < DM) -> ring d' = DM-1-d; vprog = min_d (f[d] + hoff[d])
-            int f[MAXD], ho[MAXD], rows[MAXD], hr[WMAX][MAXD], sl[MAXD];
+            int f[MAXD], ho[MAXD], rows[MAXD], hr[WMAX][MAXD], sl[MAXD], hb[MAXD];
 #pragma unroll
             for (int d = 0; d < MAXD; ++d) {
                 const int gh = g0 - 1 - d;
                 ho[d] = d < DM ? a.hoff[task * MAXD + d] : INT_MIN;
                 sl[d] = d < DM ? a.hsl[task * MAXD + d] : 0;  // ring slot of row j: (j + sl) mod RY
-                rows[d] = gh >= 0 ? int(min(int64_t(S), int64_t(n) - int64_t(gh) * S)) : 0;
+                hb[d] = gh >= 0 ? starts[gh] : 0;
+                rows[d] = gh >= 0 ? starts[gh + 1] - hb[d] : 0;
                 f[d] = (d < DM && gh >= 0 && ho[d] > INT_MIN / 2) ? 0 : rows[d];
                 for (int w = 0; w < WMAX; ++w) hr[w][d] = (w < W && d < DM) ? a.hrb[(task * W + w) * MAXD + d] : INF;
             }
@@ -309,7 +314,7 @@ __global__ void __launch_bounds__(32 * (WMAX + 2)) k_wave(WaveArgs a) {
                     for (int w = 0; w < WMAX; ++w) lim = min(lim, pr[w] >= INF ? INF : pr[w] + hr[w][d]);
                     const int j = f[d] + lane;
                     if (f[d] < rows[d] && j < rows[d] && j < lim)
-                        v[d] = ld_relaxed_nb(a.out + int64_t(g0 - 1 - d) * S + j);
+                        v[d] = ld_relaxed_nb(a.out + hb[d] + j);
                 }
                 int vp = INF;
 #pragma unroll
@@ -345,8 +350,8 @@ __global__ void __launch_bounds__(32 * (WMAX + 2)) k_wave(WaveArgs a) {
         const int nq = NS / G;
         const int k = lane / NR, rl = lane % NR, gbase = k * NR;
         const int g = b * SPW + k;
-        const int64_t lo = int64_t(g) * S;
-        const int rows = g < a.nseg ? int(min(int64_t(S), int64_t(n) - lo)) : 0;
+        const int64_t lo = g < a.nseg ? starts[g] : 0;
+        const int rows = g < a.nseg ? starts[g + 1] - starts[g] : 0;
         const int phase = (P + D * k + rl) % NR;         // lane finalises at step t <=> t % NR == phase
         const int c0 = ((-1 - P - D * k) % NR + NR) % NR;  // finaliser of step t-1: gbase + ((t + c0) % NR)
         const unsigned pred = warp == 0 ? s_vprog : s_prog + 4 * (warp - 1);
@@ -382,12 +387,23 @@ __global__ void __launch_bounds__(32 * (WMAX + 2)) k_wave(WaveArgs a) {
         group_wait(0);
         int pv = ld_acq_s(pred);
         while (pv < Lw - 1) pv = ld_acq_s(pred);  // the prologue loads below belong to step -1
-        Step cur, nxt, now;
-        fetch_item(ibase, now);
-        fetch_item(ibase + STEP_BYTES, cur);
-        double yc[4];
+        // software pipeline: items of step t+1 (cur) and t+2 (nxt); for step t, the products of
+        // its first C-1 terms (pc, computed at step t-1 from values loaded at step t-1), its last
+        // term's value / coefficient / address (y3, w3, o3) and 1/diagonal (wd)
+        Step cur, nxt;
+        double pc[3], y3, w3, wd;
+        unsigned o3;
+        {
+            Step now;
+            fetch_item(ibase, now);
+            fetch_item(ibase + STEP_BYTES, cur);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) yc[q] = lds_f64(now.o[q]);
+            for (int q = DS; q < 3; ++q) pc[q] = now.w[q] * lds_f64(now.o[q]);
+            y3 = lds_f64(now.o[3]);
+            w3 = now.w[3];
+            o3 = now.o[3];
+            wd = now.w[DS];
+        }
         double rh = lds_f64(rbase), sr = 0.0;
         if (K == kSkewGS) sr = lds_f64(sbase2);
         double acc = 0.0, x = 0.0;
@@ -404,55 +420,50 @@ __global__ void __launch_bounds__(32 * (WMAX + 2)) k_wave(WaveArgs a) {
 #pragma unroll
             for (int u = 0; u < G; ++u) {
                 const int t = tb + u;
-                // the predecessor's progress, loaded a step ago (progress only grows, so a stale
-                // value is a valid lower bound); reloaded now for the next step's test, off the chain
+                // the broadcast first: it heads the step's critical chain and touches no shared
+                // memory, so the progress test (a branch) need not come before it
+                const double xb = __shfl_sync(FULL, x, gbase + ((u + c0) & (NR - 1)));
+                // the predecessor's progress, read a step ago (it only grows, so a stale value is
+                // a valid lower bound) and re-read now, off the chain; acquire loads keep the ring
+                // loads below after the test
                 if (u % CHK == 0) {  // one test covers the loads of steps t .. t+CHK-1
                     pv = wait_ge(pred, pv, t + CHK - 1 + Lw);
                     pv = ld_acq_s(pred);
                 }
-                const double xb = __shfl_sync(FULL, x, gbase + ((u + c0) & (NR - 1)));
                 if (u == G - 2) group_wait(qg + 1);
+                // loads for step t+1 (values, items of t+2, right-hand side); their products are
+                // formed at the end of this step, so they are issued early and their latency is
+                // hidden behind this step's chain
                 double yn[4];
 #pragma unroll
                 for (int q = DS; q < 4; ++q) yn[q] = lds_f64(cur.o[q]);
                 fetch_item(ibase + ((t + 2) % PF) * STEP_BYTES, nxt);
                 const int rs = ((t + 1) % (NRH * G)) * SPW * 8;
-#ifdef PMG_DIAG_NO_RHS
-                const double rhn = 1.0;
-                (void)rs;
-#else
                 const double rhn = lds_f64(rbase + rs);
-#endif
                 double srn = 0.0;
                 if (K == kSkewGS) srn = lds_f64(sbase2 + rs);
-#ifdef PMG_DIAG_NO_XBSEL
-                const double y3 = xb;
-#else
-                const double y3 = now.o[3] == XB ? xb : yc[3];
-#endif
+                // step t: its chunk in the oracle's order, the last term from the broadcast if it
+                // is the value finalised at the previous step
                 double r = acc;
-                if (C == 4) r = r + now.w[0] * yc[0];
-                r = r + now.w[1] * yc[1];
-                r = r + now.w[2] * yc[2];
-                r = r + now.w[3] * y3;
+#pragma unroll
+                for (int q = DS; q < 3; ++q) r = r + pc[q];
+                r = r + w3 * (o3 == XB ? xb : y3);
                 const bool stage0 = (u & (NR - 1)) == phase;
                 const int ix = t - P - D * k;
-                x = K == kSkewL ? rh - r : K == kSkewU ? (rh - r) * now.w[DS] : ((rh - r) - sr) * now.w[DS];
-                // ring cells are indexed by the step that finalised the value (cells of
-                // rows outside the segment are never read); the output only for real rows
+                x = K == kSkewL ? rh - r : K == kSkewU ? (rh - r) * wd : ((rh - r) - sr) * wd;
+                // ring cells are indexed by the step that finalised the value (cells of rows
+                // outside the segment are never read); the output only for real rows
                 if (stage0) rings[rgb + u] = x;
-#ifndef PMG_DIAG_NO_STG
                 if (stage0 && ix >= 0 && ix < rows) outp[ix] = x;
-#endif
-#ifdef PMG_DIAG_NO_RESET
-                acc = r;
-#else
                 acc = stage0 ? 0.0 : r;
-#endif
                 if (u % CHK == CHK - 1) st_vol_s(s_me, t + 1);
+                // step t+1's products and last term
 #pragma unroll
-                for (int q = 0; q < 4; ++q) yc[q] = yn[q];
-                now = cur;
+                for (int q = DS; q < 3; ++q) pc[q] = cur.w[q] * yn[q];
+                y3 = yn[3];
+                w3 = cur.w[3];
+                o3 = cur.o[3];
+                wd = cur.w[DS];
                 cur = nxt;
                 rh = rhn;
                 sr = srn;
@@ -488,6 +499,17 @@ struct RowView {
     __device__ double val(int k) const { return S.val[base + (k >> 1) * 64 + li * 2 + (k & 1)]; }
 };
 
+// segment of v-row v: starts[g] <= v < starts[g+1]
+__device__ __forceinline__ int seg_of(const int32_t* __restrict__ starts, int nseg, int v) {
+    int lo = 0, hi = nseg;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (starts[mid] <= v) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
+
 // term i of a row with m terms: chunk (stage) and slot
 __device__ __forceinline__ void chunk_of(int i, int m, int C, int C0, int& s, int& q) {
     const int r = m - 1 - i;  // 0 = last term
@@ -509,11 +531,12 @@ struct PlanDev {
 
 // pass 1: validity, in-block skew D_b, reach
 template <int K>
-__global__ void k_wave_req(Sell S, const int32_t* nlow, int32_t seg, int NR, int C, PlanDev p) {
+__global__ void k_wave_req(Sell S, const int32_t* nlow, const int32_t* starts, int32_t nseg, int NR, int C,
+                           PlanDev p) {
     const int32_t v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= S.n) return;
     const int SPW = 32 / NR, P = NR - 1, C0 = K == kSkewL ? C : C - 1;
-    const int g = v / seg, ix = v - g * seg, k = g % SPW;
+    const int g = seg_of(starts, nseg, v), ix = v - starts[g], k = g % SPW;
     RowView<K> r(S, v, nlow);
     int dreq = 1, dm = 0, ring = 0, fail = 0, prev = INT_MIN;
     for (int i = 0; i < r.len; ++i) {
@@ -523,7 +546,7 @@ __global__ void k_wave_req(Sell S, const int32_t* nlow, int32_t seg, int NR, int
         int s, q;
         chunk_of(i, r.len, C, C0, s, q);
         if (s > P) fail |= 2;
-        const int gc = c / seg, jx = c - gc * seg, d = g - gc;
+        const int gc = seg_of(starts, nseg, c), jx = c - starts[gc], d = g - gc;
         if (d > MAXD) fail |= 8;
         dm = max(dm, d);
         if (d == 0) {
@@ -543,11 +566,12 @@ __global__ void k_wave_req(Sell S, const int32_t* nlow, int32_t seg, int NR, int
 
 // pass 2: leads and read-behind between blocks; in-block ring requirement
 template <int K>
-__global__ void k_wave_req2(Sell S, const int32_t* nlow, int32_t seg, int NR, int C, PlanDev p) {
+__global__ void k_wave_req2(Sell S, const int32_t* nlow, const int32_t* starts, int32_t nseg, int NR, int C,
+                            PlanDev p) {
     const int32_t v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= S.n) return;
     const int SPW = 32 / NR, P = NR - 1, C0 = K == kSkewL ? C : C - 1;
-    const int g = v / seg, ix = v - g * seg, k = g % SPW, b = g / SPW;
+    const int g = seg_of(starts, nseg, v), ix = v - starts[g], k = g % SPW, b = g / SPW;
     const int D = p.Db[b];
     RowView<K> r(S, v, nlow);
     int Rl[EMAX], Wl[EMAX];
@@ -557,7 +581,7 @@ __global__ void k_wave_req2(Sell S, const int32_t* nlow, int32_t seg, int NR, in
         const int c = r.col(i);
         int s, q;
         chunk_of(i, r.len, C, C0, s, q);
-        const int gc = c / seg, jx = c - gc * seg, d = g - gc;
+        const int gc = seg_of(starts, nseg, c), jx = c - starts[gc], d = g - gc;
         if (d == 0 || d > MAXD) continue;
         const int tload = (ix - s) + P + D * k - 1;
         if (d <= k) {
@@ -580,8 +604,8 @@ __global__ void k_wave_req2(Sell S, const int32_t* nlow, int32_t seg, int NR, in
 
 // pass 3: items, one thread per (step, lane)
 template <int K>
-__global__ void k_wave_fill(Sell S, const int32_t* __restrict__ nlow, const double* __restrict__ dinv, int32_t seg,
-                            int32_t nseg, const int32_t* __restrict__ Db, const int64_t* __restrict__ off, int32_t nblk,
+__global__ void k_wave_fill(Sell S, const int32_t* __restrict__ nlow, const double* __restrict__ dinv,
+                            const int32_t* __restrict__ starts, int32_t nseg, const int32_t* __restrict__ Db, const int64_t* __restrict__ off, int32_t nblk,
                             int NR, int C, int W, int DM, int RY, int ring0, int xb, unsigned sbase,
                             int64_t nsteps, uint4* __restrict__ item) {
     const int64_t gid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -609,8 +633,8 @@ __global__ void k_wave_fill(Sell S, const int32_t* __restrict__ nlow, const doub
         it.w[q] = 0.0;
         it.o[q] = unsigned(zero);
     }
-    if (g < nseg && ix >= 0 && ix < seg && int64_t(g) * seg + ix < S.n) {
-        const int v = g * seg + ix;
+    if (g < nseg && ix >= 0 && ix < starts[g + 1] - starts[g]) {
+        const int v = starts[g] + ix;
         RowView<K> r(S, v, nlow);
         if (s == 0 && K != kSkewL) it.w[DS] = dinv[v];
         for (int i = 0; i < r.len; ++i) {
@@ -618,7 +642,7 @@ __global__ void k_wave_fill(Sell S, const int32_t* __restrict__ nlow, const doub
             chunk_of(i, r.len, C, C0, si, q);
             if (si != s) continue;
             const int c = r.col(i);
-            const int gc = c / seg, jx = c - gc * seg, d = g - gc;
+            const int gc = seg_of(starts, nseg, c), jx = c - starts[gc], d = g - gc;
             it.w[q] = r.val(i);
             if (d == 0 && q == 3 && jx == ix - s - 1) {
                 it.o[q] = sbase + unsigned(xb);
@@ -664,11 +688,11 @@ __global__ void k_wave_upd(const double* __restrict__ x, double* __restrict__ u,
 }
 
 template <int K>
-void launch_req(const Sell& S, const int32_t* nlow, int32_t seg, int NR, int C, const PlanDev& p, bool second,
-                cudaStream_t st) {
+void launch_req(const Sell& S, const int32_t* nlow, const int32_t* starts, int32_t nseg, int NR, int C,
+                const PlanDev& p, bool second, cudaStream_t st) {
     const int nb = ceil_div(S.n, 256);
-    if (second) k_wave_req2<K><<<nb, 256, 0, st>>>(S, nlow, seg, NR, C, p);
-    else k_wave_req<K><<<nb, 256, 0, st>>>(S, nlow, seg, NR, C, p);
+    if (second) k_wave_req2<K><<<nb, 256, 0, st>>>(S, nlow, starts, nseg, NR, C, p);
+    else k_wave_req<K><<<nb, 256, 0, st>>>(S, nlow, starts, nseg, NR, C, p);
     PMG_LAUNCH_CHECK();
 }
 
@@ -713,10 +737,29 @@ bool g_wave_trace_on = false;
 unsigned long long* g_wave_trace = nullptr;
 int g_wave_trace_n = 0;
 
-bool wave_plan(const Sell& S, const double* dinv, int32_t seg, SkewKind kind, int32_t max_terms, WavePlan& plan,
-               cudaStream_t st, const int32_t* nlow) {
+std::vector<int32_t> uniform_starts(int32_t n, int32_t seg) {
+    std::vector<int32_t> v;
+    for (int64_t i = 0; i < n; i += seg) v.push_back(int32_t(i));
+    v.push_back(n);
+    return v;
+}
+
+std::vector<int32_t> reversed_starts(const std::vector<int32_t>& s) {
+    const int32_t n = s.back();
+    std::vector<int32_t> r(s.size());
+    for (size_t i = 0; i < s.size(); ++i) r[i] = n - s[s.size() - 1 - i];
+    return r;
+}
+
+bool wave_plan(const Sell& S, const double* dinv, const std::vector<int32_t>& hstarts, SkewKind kind,
+               int32_t max_terms, WavePlan& plan, cudaStream_t st, const int32_t* nlow) {
     wave_plan_free(plan);
-    if (seg <= 0 || S.n == 0) return false;
+    if (S.n == 0 || hstarts.size() < 2 || hstarts.front() != 0 || hstarts.back() != S.n) return false;
+    int32_t seg = 0;  // longest segment
+    for (size_t i = 0; i + 1 < hstarts.size(); ++i) {
+        if (hstarts[i + 1] <= hstarts[i]) return false;
+        seg = std::max(seg, hstarts[i + 1] - hstarts[i]);
+    }
     static const int lay[][2] = {{4, 3}, {8, 4}, {16, 4}, {32, 3}, {32, 4}};
     const int extra = kind == kSkewL ? 0 : 1;  // chunk 0 carries 1/diagonal
     int NR = 0, C = 0;
@@ -729,14 +772,18 @@ bool wave_plan(const Sell& S, const double* dinv, int32_t seg, SkewKind kind, in
     if (!NR) return false;
     const bool verbose = getenv("PMG_VERBOSE") != nullptr;
     const int SPW = 32 / NR, P = NR - 1;
-    const int nseg = ceil_div(S.n, seg);
+    const int nseg = int(hstarts.size()) - 1;
     const int nblk = ceil_div(nseg, SPW);
+    int32_t* starts = nullptr;
+    PMG_CUDA(cudaMalloc(&starts, sizeof(int32_t) * (nseg + 1)));
+    PMG_CUDA(cudaMemcpyAsync(starts, hstarts.data(), sizeof(int32_t) * (nseg + 1), cudaMemcpyHostToDevice, st));
     PlanDev p{};
     PMG_CUDA(cudaMalloc(&p.Db, sizeof(int32_t) * nblk));
     PMG_CUDA(cudaMalloc(&p.R, sizeof(int32_t) * nblk * EMAX));
     PMG_CUDA(cudaMalloc(&p.Wb, sizeof(int32_t) * nblk * EMAX));
     PMG_CUDA(cudaMalloc(&p.out, sizeof(int) * 4));
     auto release = [&] {
+        cudaFree(starts);
         cudaFree(p.Db);
         cudaFree(p.R);
         cudaFree(p.Wb);
@@ -748,9 +795,9 @@ bool wave_plan(const Sell& S, const double* dinv, int32_t seg, SkewKind kind, in
     PMG_CUDA(cudaMemcpyAsync(p.Wb, minus.data(), sizeof(int32_t) * minus.size(), cudaMemcpyHostToDevice, st));
     PMG_CUDA(cudaMemsetAsync(p.out, 0, sizeof(int) * 4, st));
     auto req = [&](bool second) {
-        if (kind == kSkewL) launch_req<kSkewL>(S, nlow, seg, NR, C, p, second, st);
-        else if (kind == kSkewU) launch_req<kSkewU>(S, nlow, seg, NR, C, p, second, st);
-        else launch_req<kSkewGS>(S, nlow, seg, NR, C, p, second, st);
+        if (kind == kSkewL) launch_req<kSkewL>(S, nlow, starts, nseg, NR, C, p, second, st);
+        else if (kind == kSkewU) launch_req<kSkewU>(S, nlow, starts, nseg, NR, C, p, second, st);
+        else launch_req<kSkewGS>(S, nlow, starts, nseg, NR, C, p, second, st);
     };
     req(false);
     int h[4];
@@ -852,6 +899,8 @@ bool wave_plan(const Sell& S, const double* dinv, int32_t seg, SkewKind kind, in
     std::vector<int64_t> hoff(nblk + 1, 0);
     for (int b = 0; b < nblk; ++b) {
         const int kl = std::min(SPW - 1, nseg - 1 - b * SPW);
+        int32_t seg = 0;  // the block's longest segment
+        for (int k = 0; k <= kl; ++k) seg = std::max(seg, hstarts[b * SPW + k + 1] - hstarts[b * SPW + k]);
         // whole groups, at least NG (the last steps fetch items one group past the end: the
         // ring slot then still holds valid offsets of an earlier group)
         const int64_t ns = std::max<int64_t>(seg + int64_t(kl) * hD[b] + P, NG * G);
@@ -879,13 +928,13 @@ bool wave_plan(const Sell& S, const double* dinv, int32_t seg, SkewKind kind, in
     const int nf = ceil_div(nsteps * 32, 256);
     const unsigned sbase = dyn_smem_base(st);
     if (kind == kSkewL)
-        k_wave_fill<kSkewL><<<nf, 256, 0, st>>>(S, nlow, dinv, seg, nseg, p.Db, offd, nblk, NR, C, W, dm, ry, ly.ring,
+        k_wave_fill<kSkewL><<<nf, 256, 0, st>>>(S, nlow, dinv, starts, nseg, p.Db, offd, nblk, NR, C, W, dm, ry, ly.ring,
                                                 ly.xb, sbase, nsteps, item);
     else if (kind == kSkewU)
-        k_wave_fill<kSkewU><<<nf, 256, 0, st>>>(S, nlow, dinv, seg, nseg, p.Db, offd, nblk, NR, C, W, dm, ry, ly.ring,
+        k_wave_fill<kSkewU><<<nf, 256, 0, st>>>(S, nlow, dinv, starts, nseg, p.Db, offd, nblk, NR, C, W, dm, ry, ly.ring,
                                                 ly.xb, sbase, nsteps, item);
     else
-        k_wave_fill<kSkewGS><<<nf, 256, 0, st>>>(S, nlow, dinv, seg, nseg, p.Db, offd, nblk, NR, C, W, dm, ry,
+        k_wave_fill<kSkewGS><<<nf, 256, 0, st>>>(S, nlow, dinv, starts, nseg, p.Db, offd, nblk, NR, C, W, dm, ry,
                                                  ly.ring, ly.xb, sbase, nsteps, item);
     PMG_LAUNCH_CHECK();
     PMG_CUDA(cudaStreamSynchronize(st));
@@ -897,6 +946,7 @@ bool wave_plan(const Sell& S, const double* dinv, int32_t seg, SkewKind kind, in
     plan.n = S.n;
     plan.seg = seg;
     plan.nseg = nseg;
+    plan.starts = starts;
     plan.nr = NR;
     plan.c = C;
     plan.spw = SPW;
@@ -924,6 +974,7 @@ bool wave_plan(const Sell& S, const double* dinv, int32_t seg, SkewKind kind, in
 }
 
 void wave_plan_free(WavePlan& plan) {
+    cudaFree(plan.starts);
     cudaFree(plan.Db);
     cudaFree(plan.Lb);
     cudaFree(plan.bp);
@@ -968,6 +1019,7 @@ void wave_sweep(const WaveOp& op, int* ticket, cudaStream_t st) {
         PMG_LAUNCH_CHECK();
     }
     WaveArgs a{};
+    a.starts = p.starts;
     a.item = p.item;
     a.rhs = op.rhs;
     a.su = op.su;

@@ -3,6 +3,8 @@
 // fit a layout.  See wave.cu for the design; skew.cu / chain.cu / trsv.cu remain as fallbacks.
 #pragma once
 
+#include <vector>
+
 #include "skew.cuh"
 
 namespace pmg {
@@ -10,7 +12,8 @@ namespace pmg {
 // Per-(block, step, lane) items (4 coefficients + 4 shared-memory byte offsets, 48 B) stored
 // step-major per warp block; a CTA runs `w` consecutive blocks (one sweep warp each).
 struct WavePlan {
-    int32_t n = 0, seg = 0, nseg = 0;
+    int32_t n = 0, seg = 0, nseg = 0;  // seg: longest segment
+    int32_t* starts = nullptr;   // [nseg+1] first v-row of every segment (device)
     int32_t nr = 4, c = 3;       // lanes per segment, terms per lane and step
     int32_t spw = 8, w = 1;      // segments per warp block, warp blocks per CTA
     int32_t nblk = 0, ntask = 0; // warp blocks, CTA tasks
@@ -30,11 +33,14 @@ struct WavePlan {
     bool ok = false;
 };
 
-// Build the plan of the v-ordered matrix S (kinds and arguments as skew_plan).  Returns false
-// (nothing allocated) if a row does not fit the widest layout, reaches more than 8 segments
-// back, or the rings do not fit shared memory.
-bool wave_plan(const Sell& S, const double* dinv, int32_t seg, SkewKind kind, int32_t max_terms, WavePlan& plan,
-               cudaStream_t st, const int32_t* nlow = nullptr);
+// Build the plan of the v-ordered matrix S (kinds and arguments as skew_plan); segments (grid
+// rows, any lengths) are given by their first v-rows, starts.back() == n.  Returns false (nothing
+// allocated) if a row does not fit the widest layout, reaches more than 8 segments back, or the
+// rings do not fit shared memory.
+bool wave_plan(const Sell& S, const double* dinv, const std::vector<int32_t>& starts, SkewKind kind,
+               int32_t max_terms, WavePlan& plan, cudaStream_t st, const int32_t* nlow = nullptr);
+std::vector<int32_t> uniform_starts(int32_t n, int32_t seg);
+std::vector<int32_t> reversed_starts(const std::vector<int32_t>& starts);  // natural -> descending v-order
 void wave_plan_free(WavePlan& plan);
 
 struct WaveOp {

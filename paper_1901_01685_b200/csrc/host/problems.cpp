@@ -197,6 +197,10 @@ int iga_config_spec(int config, int degree, iga_problem_spec* s) {
         case 4:
             s->geometry = IGA_GEOM_LSHAPE; s->rhs = IGA_RHS_ONE; s->h_exp = 8;
             s->n_degrees = 2; s->degrees[0] = 4; s->degrees[1] = 1;
+            // global row-major DOF numbering over the L-shape's control grid (SPEC.md:44-49 leaves
+            // multipatch numbering open): every grid row is one contiguous segment, so the
+            // triangular sweeps keep their wavefront across the patch interfaces
+            s->numbering = IGA_NUMBER_ROWMAJOR;
             break;
         case 5:
             s->geometry = IGA_GEOM_ANNULUS; s->rhs = IGA_RHS_ANNULUS; s->h_exp = 10;

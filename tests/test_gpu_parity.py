@@ -297,3 +297,31 @@ def test_p1_only_hierarchy_converges():
     assert ro["converged"] and rep.converged
     assert rep.cycles == ro["cycles"] < 20
     assert_bitwise(u, uo, "p=1-only solve")
+
+
+@pytest.mark.parametrize("p,h_exp", [(1, 5), (2, 5), (4, 5), (4, 6)])
+def test_wave_variable_segments_lshape(p, h_exp):
+    """Rotating-lane sweeps on grid rows of different lengths: the L-shape (3 patches) in global
+    row-major numbering has rows of 2n-1 DOFs below y = 0 and n above (segments detected from the
+    pattern).  ILUT apply and the GS sweep, bitwise against the oracle."""
+    pb = P.build(P.make_spec(geometry="lshape", rhs="one", degrees=(max(p, 2), 1), h_exp=h_exp, numbering="rowmajor"))
+    A = pb.hlevels[0].A if p == 1 else pb.plevels[0].A
+    Fg = pmg.ilut_factorize(A, 1e-12, 1.0, "none")
+    assert Fg.stats()["sweep"] == "wave", Fg.stats()
+    Fo = O.ilut_factorize(A, 1e-12, 1.0, O.ORDER_NONE)
+    rng = np.random.default_rng(p)
+    r = rng.uniform(-1, 1, A.nrows)
+    assert_bitwise(pmg.ilut_apply(Fg, r), Fo.apply(r), "wave ilut_apply (variable segments)")
+    u, f = rng.uniform(-1, 1, A.nrows), rng.uniform(-1, 1, A.nrows)
+    assert_bitwise(pmg.gauss_seidel_sweep(A, u, f), O.gauss_seidel_sweep(A, u, f), "wave GS (variable segments)")
+
+
+def test_solve_lshape_rowmajor():
+    """A whole p-MG solve on the row-major L-shape (config 4's numbering at h = 2^-5), bitwise."""
+    pb = P.build(P.make_spec(geometry="lshape", rhs="one", degrees=(4, 1), h_exp=5, numbering="rowmajor"))
+    Hg = pmg.build_hierarchy(pb, smoother="ilut")
+    assert all(F.stats()["sweep"] == "wave" for F in Hg.factors())
+    u, rep = pmg.solve(Hg, pb.f, guess=pb.u0)
+    uo, ro = O.Hierarchy(pb, smoother=O.ILUT).solve(pb.f, pb.u0)
+    assert rep.cycles == ro["cycles"] and rep.converged
+    assert_bitwise(u, uo, "L-shape row-major solve")
