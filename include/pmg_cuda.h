@@ -134,6 +134,12 @@ int pmg_bicgstab_device(pmg_work W, const double* d_f, double* d_u, double tol, 
                         int* iters, int* flags, double* solve_seconds);
 /* one cycle at p-level `level` on host vectors (u updated in place) */
 int pmg_cycle(pmg_work W, int level, double* u, const double* f);
+/* one smoothing step (ILUT or GS, the hierarchy's smoother; p = 1: the ILUT smoother of the
+ * finest h-level) / one coarse-grid correction (restrict f - A u, one cycle at level+1 from
+ * zero, prolongate and add: PAPER §4 steps 2-4) at p-level `level`, host vectors, u in place.
+ * The two halves of the cycle that reduction_factors applies separately. */
+int pmg_smooth(pmg_work W, int level, double* u, const double* f);
+int pmg_coarse_correction(pmg_work W, int level, double* u, const double* f);
 /* prolongate: v_fine = ML_l^-1 P_l v_coarse; restrict */
 int pmg_prolongate(pmg_hier H, int level, const double* v_coarse, double* v_fine);
 int pmg_restrict(pmg_hier H, int level, const double* r_fine, double* r_coarse);

@@ -1011,4 +1011,34 @@ int orc_cycle(orc_hier h, int level, double* u, const double* f) {
     return e >= 0 ? PMG_ZERO_DIAG : PMG_OK;
 }
 
+// one smoothing step at p-level `level` (p = 1: the finest h-level's ILUT smoother), and one
+// coarse-grid correction (PAPER §4 steps 2-4: restrict f - A u, one cycle at level+1 from zero,
+// prolongate and add) -- the halves of the cycle reduction_factors applies
+int orc_smooth(orc_hier h, int level, double* u, const double* f) {
+    Hier& H = h->H;
+    if (level < 0 || level >= H.np) return PMG_ERR_ARG;
+    if (level == H.np - 1) {
+        HLev& L = H.hl[0];
+        PLev& P = H.pl[level];
+        if (!L.F) return PMG_ERR_ARG;  // p = 1 level is the dense coarsest level itself
+        ilut_smooth(*L.A, *L.F, u, f, nullptr, P.r.data(), L.y.data(), L.x.data());
+        return PMG_OK;
+    }
+    return smooth(H, level, u, f, nullptr) >= 0 ? PMG_ZERO_DIAG : PMG_OK;
+}
+
+int orc_coarse_correction(orc_hier h, int level, double* u, const double* f) {
+    Hier& H = h->H;
+    if (level < 0 || level >= H.np - 1) return PMG_ERR_ARG;
+    PLev& L = H.pl[level];
+    PLev& C = H.pl[level + 1];
+    residual(L.A, u, f, L.r.data());
+    restrict_(L.PT, C.ML.data(), L.r.data(), C.f.data());
+    std::fill(C.u.begin(), C.u.end(), 0.0);
+    int64_t e = vcycle(H, level + 1, C.u.data(), C.f.data(), nullptr, true);
+    if (e >= 0) return PMG_ZERO_DIAG;
+    prolong_add(L.P, L.ML.data(), C.u.data(), u);
+    return PMG_OK;
+}
+
 }  // extern "C"

@@ -66,6 +66,8 @@ orc_factor orc_hier_factor(orc_hier H, int which);
 int orc_solve(orc_hier H, const double* f, double* u, double tol, int max_cycles, double* rho_hist, int* cycles,
               int* flags, double* solve_seconds, double* setup_seconds);
 int orc_cycle(orc_hier H, int level, double* u, const double* f);
+int orc_smooth(orc_hier H, int level, double* u, const double* f);
+int orc_coarse_correction(orc_hier H, int level, double* u, const double* f);
 /* right-preconditioned BiCGSTAB, one V-cycle from zero per preconditioning;
  * hist needs max_iter+1 entries; flags: PMG_FLAG_CONVERGED / DIVERGED / BREAKDOWN */
 int orc_bicgstab(orc_hier H, const double* f, double* u, double tol, int max_iter, double* hist, int* iters, int* flags,

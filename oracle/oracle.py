@@ -67,6 +67,8 @@ def lib():
         L.orc_hier_factor.restype = vp
         L.orc_solve.argtypes = [vp, vp, vp, dbl, ctypes.c_int, vp, vp, vp, vp, vp]
         L.orc_cycle.argtypes = [vp, ctypes.c_int, vp, vp]
+        L.orc_smooth.argtypes = [vp, ctypes.c_int, vp, vp]
+        L.orc_coarse_correction.argtypes = [vp, ctypes.c_int, vp, vp]
         L.orc_bicgstab.argtypes = [vp, vp, vp, dbl, ctypes.c_int, vp, vp, vp, vp]
         L.orc_bicgstab_plain.argtypes = [vp, vp, vp, dbl, ctypes.c_int, vp, vp, vp]
         L.orc_dot.restype = dbl
@@ -311,4 +313,20 @@ class Hierarchy:
     def cycle(self, u, f, level=0):
         u = np.array(u, dtype=float, copy=True)
         lib().orc_cycle(self.h, level, _p(u), _p(np.ascontiguousarray(f, float)))
+        return u
+
+    def smooth(self, u, f, level=0):
+        """One smoothing step at p-level `level` (reduction_factors)."""
+        u = np.array(u, dtype=float, copy=True)
+        st = lib().orc_smooth(self.h, level, _p(u), _p(np.ascontiguousarray(f, float)))
+        if st != PMG_OK:
+            raise OracleError(st)
+        return u
+
+    def coarse_correction(self, u, f, level=0):
+        """One coarse-grid correction at p-level `level` (PAPER §4 steps 2-4)."""
+        u = np.array(u, dtype=float, copy=True)
+        st = lib().orc_coarse_correction(self.h, level, _p(u), _p(np.ascontiguousarray(f, float)))
+        if st != PMG_OK:
+            raise OracleError(st)
         return u

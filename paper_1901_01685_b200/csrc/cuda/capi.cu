@@ -1430,6 +1430,55 @@ int pmg_cycle(pmg_work W, int level, double* u, const double* f) {
     });
 }
 
+// One smoothing step (GS: SPEC.md:233-241) or one coarse-grid correction
+// (steps 2-4 of the cycle, PAPER §4 "referred to as 'coarse grid correction'": restrict the
+// residual, one cycle at level+1 from zero, prolongate and add) at p-level `level`, on host
+// vectors; the building blocks of reduction_factors.
+static int part_step(pmg_work W, int level, double* u, const double* f, bool cgc) {
+    return guarded([&] {
+        pmg_hier_s& H = *W->H;
+        const int top = int(H.pl.size()) - 1 - (cgc ? 1 : 0);
+        if (level < 0 || level > top) throw ArgError(cgc ? "coarse_correction: bad level" : "smooth: bad level", PMG_ERR_ARG);
+        PLev& L = H.pl[level];
+        const int32_t n = L.A->A.n;
+        PWork& w = W->pw[level];
+        w.cur = 0;
+        HostVecs hv;
+        double* df = hv.make(n);
+        PMG_CUDA(cudaMemcpyAsync(df, f, sizeof(double) * n, cudaMemcpyHostToDevice, W->st));
+        PMG_CUDA(cudaMemcpyAsync(w.u[0], u, sizeof(double) * n, cudaMemcpyHostToDevice, W->st));
+        int rc = PMG_OK;
+        if (!cgc) {
+            if (level == int(H.pl.size()) - 1) {  // p = 1: the ILUT smoother of the finest h-level
+                HLev& hl = H.hl[0];
+                if (!hl.F) throw ArgError("smooth: the p = 1 level is the dense coarsest level", PMG_ERR_ARG);
+                smooth_ilut(*W, hl.A, hl.F, w.u[0], df, nullptr, w.r, w.y, w.x, false);
+            } else {
+                rc = smooth(*W, level, df, nullptr);
+            }
+        } else {
+            PLev& C = H.pl[level + 1];
+            PWork& c = W->pw[level + 1];
+            W->run(kClsResid0, 1, [&] { sell_rowop(L.A->S, kOpResidual, w.u[0], df, nullptr, w.r, nullptr, W->st); });
+            W->run(kClsTransfer, 1, [&] { sell_rowop(L.PT->S, kOpRestrict, w.r, nullptr, C.ML, c.f, nullptr, W->st); });
+            PMG_CUDA(cudaMemsetAsync(c.u[c.cur], 0, sizeof(double) * C.A->A.n, W->st));
+            rc = vcycle(*W, level + 1, c.f, nullptr, true);
+            if (!rc)
+                W->run(kClsTransfer, 1,
+                       [&] { sell_rowop(L.P->S, kOpProlongAdd, c.u[c.cur], nullptr, L.ML, w.u[0], nullptr, W->st); });
+        }
+        PMG_CUDA(cudaMemcpyAsync(u, w.u[w.cur], sizeof(double) * n, cudaMemcpyDeviceToHost, W->st));
+        PMG_CUDA(cudaStreamSynchronize(W->st));
+        return rc;
+    });
+}
+
+int pmg_smooth(pmg_work W, int level, double* u, const double* f) { return part_step(W, level, u, f, false); }
+
+int pmg_coarse_correction(pmg_work W, int level, double* u, const double* f) {
+    return part_step(W, level, u, f, true);
+}
+
 int pmg_prolongate(pmg_hier H, int level, const double* vc, double* vf) {
     return guarded([&] {
         if (level < 0 || level + 1 >= int(H->pl.size())) throw ArgError("prolongate: bad level", PMG_ERR_ARG);

@@ -112,6 +112,8 @@ def lib():
         L.pmg_solve.argtypes = [vp, vp, vp, dbl, ci, vp, vp, vp, vp]
         L.pmg_solve_device.argtypes = [vp, vp, vp, dbl, ci, vp, vp, vp, vp]
         L.pmg_cycle.argtypes = [vp, ci, vp, vp]
+        L.pmg_smooth.argtypes = [vp, ci, vp, vp]
+        L.pmg_coarse_correction.argtypes = [vp, ci, vp, vp]
         L.pmg_bicgstab.argtypes = [vp, vp, vp, dbl, ci, vp, vp, vp, vp]
         L.pmg_bicgstab_device.argtypes = [vp, vp, vp, dbl, ci, vp, vp, vp, vp]
         L.pmg_prolongate.argtypes = [vp, ci, vp, vp]
@@ -428,6 +430,24 @@ def cycle(hier: PmgHierarchy, level: int, u, f):
     u = np.array(_f64(u), copy=True)
     with hier.work() as w:
         _raise(lib().pmg_cycle(w, level, ptr(u), ptr(_f64(f, u.size))), what="cycle")
+    return u
+
+
+def smooth(hier: PmgHierarchy, level: int, u, f):
+    """One smoothing step at p-level `level` (the hierarchy's smoother; the building block of
+    reduction_factors, SPEC.md:431-440)."""
+    u = np.array(_f64(u), copy=True)
+    with hier.work() as w:
+        _raise(lib().pmg_smooth(w, level, ptr(u), ptr(_f64(f, u.size))), what="smooth")
+    return u
+
+
+def coarse_correction(hier: PmgHierarchy, level: int, u, f):
+    """One coarse-grid correction at p-level `level`: restrict f - A u, one cycle at level+1 from
+    zero, prolongate and add (PAPER §4, steps 2-4 of the cycle)."""
+    u = np.array(_f64(u), copy=True)
+    with hier.work() as w:
+        _raise(lib().pmg_coarse_correction(w, level, ptr(u), ptr(_f64(f, u.size))), what="coarse_correction")
     return u
 
 

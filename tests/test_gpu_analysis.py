@@ -42,3 +42,49 @@ def test_spectral_radius_benchmark2_ilut_small():
     H = pmg.build_hierarchy(pb, smoother="ilut")
     rho = analysis.spectral_radius(analysis.iteration_matrix(H, workers=8)).rho
     assert rho < 0.2, rho
+
+
+@pytest.mark.parametrize("smoother,degrees", [("ilut", (3, 2, 1)), ("gs", (3, 2, 1)), ("ilut", (2, 1))])
+def test_smooth_and_coarse_correction_equal_oracle(smoother, degrees):
+    """pmg_smooth / pmg_coarse_correction (the halves of the cycle) are bitwise
+    equal to the oracle's at every p-level, including the p = 1 level (h-level 0 ILUT smoother)."""
+    p = degrees[0]
+    spec = P.benchmark_spec(1, p, 4, consecutive=len(degrees) > 2)
+    pb = P.build(spec)
+    H = pmg.build_hierarchy(pb, smoother=smoother)
+    Ho = O.Hierarchy(pb, smoother=O.ILUT if smoother == "ilut" else O.GS)
+    rng = np.random.default_rng(1)
+    for level, lev in enumerate(pb.plevels):
+        n = lev.A.nrows
+        u = rng.uniform(-1, 1, n)
+        f = rng.uniform(-1, 1, n)
+        np.testing.assert_array_equal(_bits(pmg.smooth(H, level, u, f)), _bits(Ho.smooth(u, f, level)))
+        if level + 1 < len(pb.plevels):
+            np.testing.assert_array_equal(_bits(pmg.coarse_correction(H, level, u, f)),
+                                          _bits(Ho.coarse_correction(u, f, level)))
+    with pytest.raises(pmg.PmgError):
+        pmg.coarse_correction(H, len(pb.plevels) - 1, np.zeros(pb.plevels[-1].A.nrows), np.zeros(pb.plevels[-1].A.nrows))
+
+
+def test_reduction_factors_benchmark1_p4():
+    """SPEC.md:437 on the GPU path: Benchmark 1, p=4, h=2^-5 -- the max GS smoother factor over the
+    upper half of the spectrum is >= 10x ILUT's; every factor equals the one computed from the
+    oracle's smoothing step / coarse-grid correction (the same arithmetic, bit for bit)."""
+    pb = P.build(P.benchmark_spec(1, 4, 5))
+    n = pb.n
+    E = analysis.generalized_eigs(pb.plevels[0].A, P.matrix("M", geometry="annulus", p=4, nel=32))
+    out = {}
+    for sm in ("ilut", "gs"):
+        H = pmg.build_hierarchy(pb, smoother=sm)
+        out[sm] = analysis.reduction_factors(H, E, "smoother", workers=4).factors
+        if sm == "ilut":
+            cg = analysis.reduction_factors(H, E, "cgc", workers=4)
+            Ho = O.Hierarchy(pb, smoother=O.ILUT)
+            f = np.zeros(n)
+            sel = np.arange(0, n, 37)
+            ref = analysis._reduction(lambda v: Ho.coarse_correction(v, f), E.eigenvectors, sel, 1)
+            np.testing.assert_array_equal(cg.factors[sel], ref)
+            assert cg.factors[:10].max() < 0.5
+    assert out["gs"][n // 2:].max() >= 10 * out["ilut"][n // 2:].max()
+    with pytest.raises(ValueError):
+        analysis.reduction_factors(H, E, "both")
