@@ -38,6 +38,9 @@ def parse():
     ap.add_argument("--degree", type=int, default=0)
     ap.add_argument("--smoother", choices=["ilut", "gs"], default="ilut")
     ap.add_argument("--ordering", choices=["none", "rcm"], default="none")
+    ap.add_argument("--assembly", choices=["gpu", "host"], default="gpu",
+                    help="who produces the matrix values of A_k, M_k, P^k_j (F2): pmg_asm_values on the GPU or the host loop")
+    ap.add_argument("--time-host-assembly", action="store_true", help="also time the host assembler (untimed setup figure)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-bicgstab", action="store_true", help="skip the BiCGSTAB sub-measurement")
     ap.add_argument("--cpu-sample-cycles", type=int, default=0, help="0: a full oracle solve")
@@ -260,8 +263,13 @@ def main():
     torch.cuda.set_device(local)
     P.set_threads(max(1, (os.cpu_count() or 1) // max(ws, 1)))
     t0 = time.perf_counter()
-    pb = P.build(args.config, args.degree)
+    pb = P.build(args.config, args.degree, assembly=args.assembly)
     t_asm = time.perf_counter() - t0
+    t_asm_host = None
+    if args.time_host_assembly and args.assembly == "gpu" and rank == 0:
+        t0 = time.perf_counter()
+        P.build(args.config, args.degree)
+        t_asm_host = time.perf_counter() - t0
     n = pb.n
     H = pmg.build_hierarchy(pb, smoother=args.smoother, ordering=args.ordering)
     d_f = torch.from_numpy(pb.f).cuda()
@@ -387,7 +395,8 @@ def main():
                    "h_levels": len(pb.hlevels), "cycles_per_solve": cycles / args.steps,
                    "final_rho": float(rep.residual_history[-1]), "converged": bool(rep.converged),
                    "l2_flush": "inputs larger than L2 (A_p alone is %.2f GB)" % (12 * pb.plevels[0].A.nnz / 1e9),
-                   "parallelism": f"replicas x{ws}", "assembly_s": round(t_asm, 2),
+                   "parallelism": f"replicas x{ws}", "assembly": args.assembly, "assembly_s": round(t_asm, 2),
+                   "host_assembly_s": None if t_asm_host is None else round(t_asm_host, 2),
                    "setup_s": round(H.setup_seconds, 3), "gpu_ilut_s": round(H.ilut_seconds, 3)},
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": 8 * n,
                 "ms_per_step": 1e3 * T_e2e / args.steps},

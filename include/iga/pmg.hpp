@@ -135,18 +135,22 @@ PmgHierarchy build_hierarchy(const HierarchyInputs& in, Smoother smoother = Smoo
                              Ordering ordering = Ordering::none);
 
 // The problem side of SPEC.md:327's build_hierarchy(spec, p, h, ...): the benchmark / geometry,
-// coefficients, degree list and h of iga_problem_spec (include/iga_host.h), assembled on the
-// host by libiga_host.so (input generation, not the solve path).
+// coefficients, degree list and h of iga_problem_spec (include/iga_host.h).  Numbering, sparsity
+// patterns and the load vector come from libiga_host.so; the matrix values of A_k, M_k, P^k_j
+// (assemble_system / assemble_mass / assemble_transfer) from the host element loop
+// or from the GPU assembler (pmg_asm_values) -- bit-identical either way.
 using ProblemSpec = iga_problem_spec;
+enum class Assembly { host, gpu };
 struct Problem {
     HierarchyInputs inputs;
     Vector f, u0;  // load vector and initial guess
 };
 ProblemSpec config_spec(int config, int degree = 0);  // BASELINE.json config 1..5 (degree: config 2's p)
-Problem assemble(const ProblemSpec& spec);
+Problem assemble(const ProblemSpec& spec, Assembly assembly = Assembly::host);
 // assemble + build_hierarchy in one call (build_hierarchy(spec, p, h, smoother, nu1, nu2))
 PmgHierarchy build_hierarchy(const ProblemSpec& spec, Smoother smoother = Smoother::ilut, int nu1 = 1, int nu2 = 1,
-                             double tau = 1e-12, double fillfactor = 1.0, Ordering ordering = Ordering::none);
+                             double tau = 1e-12, double fillfactor = 1.0, Ordering ordering = Ordering::none,
+                             Assembly assembly = Assembly::host);
 Vector prolongate(const PmgHierarchy& H, int level, const Vector& v_coarse);
 Vector restrict(const PmgHierarchy& H, int level, const Vector& r_fine);
 // (`restrict` is a C99 keyword, not a C++ one; the former spelling stays as an alias)

@@ -14,6 +14,8 @@
 
 #include <stdint.h>
 
+#include "pmg_asm.h"
+
 #ifdef __cplusplus
 extern "C" {
 #endif
@@ -50,6 +52,10 @@ void iga_set_num_threads(int n);
 /* fill *s with BASELINE.json config `config` (1..5); `degree` selects p for config 2 */
 int iga_config_spec(int config, int degree, iga_problem_spec* s);
 int iga_problem_build(const iga_problem_spec* s, iga_problem** out);
+/* F2: the same build with the matrix VALUES produced by `values` (pmg_asm_values of
+ * libpmg_cuda.so: GPU assembly); the host keeps numbering, patterns, tables,
+ * the load vector, transposes and the h-chain prolongations.  NULL = host element loop. */
+int iga_problem_build_with(const iga_problem_spec* s, pmg_asm_values_fn values, iga_problem** out);
 void iga_problem_free(iga_problem* h);
 
 int iga_problem_num_plevels(const iga_problem* h);
@@ -67,6 +73,9 @@ int iga_problem_vec_copy(const iga_problem* h, int kind, int l, double* out);
  * 2 = transfer P^p_{p2}, 3 = mass + lumped mass (IGA_VEC_ML); read it back as p-level 0 */
 int iga_matrix_build(int kind, int geometry, int p, int p2, int nel, const double* D, const double* v, double R,
                      double nitsche_scale, iga_problem** out);
+
+int iga_matrix_build_with(int kind, int geometry, int p, int p2, int nel, const double* D, const double* v, double R,
+                          double nitsche_scale, pmg_asm_values_fn values, iga_problem** out);
 
 /* MatrixMarket I/O.  Reading accepts coordinate real / integer / pattern
  * matrices, general / symmetric / skew-symmetric (mirrored), and returns sorted CSR with duplicates

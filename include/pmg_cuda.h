@@ -23,6 +23,8 @@
 
 #include <stdint.h>
 
+#include "pmg_asm.h"
+
 #ifdef __cplusplus
 extern "C" {
 #endif
@@ -147,6 +149,13 @@ int pmg_restrict(pmg_hier H, int level, const double* r_fine, double* r_coarse);
 /* timing helpers for the bench: run `cycles` V-cycles from the state left by the last
  * pmg_solve_device call and report per-kernel-class device time (ms). */
 int pmg_work_kernel_times(pmg_work W, double* ms_by_class, int n_classes);
+
+/* ---- discretization: GPU assembly of matrix values (F2) ----
+ * assemble_system / assemble_mass / assemble_transfer: the values of one operator on the sparsity
+ * pattern and tables of the request (include/pmg_asm.h), element matrices by sum factorisation and a
+ * deterministic gather; bit-identical to the host element loop of libiga_host.so.
+ * Matches pmg_asm_values_fn: pass it to iga_problem_build_with (include/iga_host.h). */
+int pmg_asm_values(const pmg_asm_request* req);
 
 /* diagnostics: mode 1/0 enables/disables per-segment globaltimer tracing of the chained
  * sweeps; mode -1 copies the trace of the last sweep (6 u64 per segment: claim, helpers done,

@@ -201,9 +201,9 @@ ProblemSpec config_spec(int config, int degree) {
     return s;
 }
 
-Problem assemble(const ProblemSpec& spec) {
+Problem assemble(const ProblemSpec& spec, Assembly assembly) {
     iga_problem* h = nullptr;
-    if (iga_problem_build(&spec, &h)) host_fail("assemble");
+    if (iga_problem_build_with(&spec, assembly == Assembly::gpu ? &pmg_asm_values : nullptr, &h)) host_fail("assemble");
     std::unique_ptr<iga_problem, void (*)(iga_problem*)> guard(h, iga_problem_free);
     Problem pb;
     const int np = iga_problem_num_plevels(h), nh = iga_problem_num_hlevels(h);
@@ -233,8 +233,8 @@ Problem assemble(const ProblemSpec& spec) {
 }
 
 PmgHierarchy build_hierarchy(const ProblemSpec& spec, Smoother smoother, int nu1, int nu2, double tau,
-                             double fillfactor, Ordering ordering) {
-    return build_hierarchy(assemble(spec).inputs, smoother, nu1, nu2, tau, fillfactor, ordering);
+                             double fillfactor, Ordering ordering, Assembly assembly) {
+    return build_hierarchy(assemble(spec, assembly).inputs, smoother, nu1, nu2, tau, fillfactor, ordering);
 }
 
 double PmgHierarchy::setup_seconds() const {

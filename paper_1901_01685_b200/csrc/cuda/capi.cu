@@ -26,6 +26,11 @@ using namespace pmg;
 
 namespace {
 thread_local std::string g_err;
+}
+namespace pmg {
+void set_last_error(const std::string& m) { g_err = m; }  // for the other translation units (assemble.cu)
+}
+namespace {
 
 struct ArgError : std::runtime_error {
     int status;

@@ -25,6 +25,9 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr unsigned FULL = 0xffffffffu;
+// candidates of a selection are also kept in shared memory when they fit (the selection after the
+// last pivot is on the row-to-row critical path: no L2 round trips there)
+constexpr int kCandSh = 1024;
 
 struct IlutDev {
     int32_t n, M, b, W, nwords;
@@ -79,7 +82,7 @@ __device__ __forceinline__ int block_scan_excl(int v, int* sh, int& total) {
 // gather the band entries [lo, hi) that are present (and, if filter, |w| >= tau) into the
 // candidate arrays in ascending order; returns the count
 __device__ int gather(const double* w, const uint32_t* pres, int lo, int hi, bool filter, double tau, int col0,
-                      int32_t* ccol, double* cval, int* sh) {
+                      int32_t* ccol, double* cval, int32_t* scol, double* sval, int* sh) {
     int base = 0;
     const int w0 = lo >> 5, w1 = (hi + 31) >> 5;
     for (int wb = w0; wb < w1; wb += kThreads) {
@@ -106,6 +109,10 @@ __device__ int gather(const double* w, const uint32_t* pres, int lo, int hi, boo
             bits &= bits - 1;
             ccol[o] = col0 + wi * 32 + q;
             cval[o] = w[wi * 32 + q];
+            if (o < kCandSh) {
+                scol[o] = col0 + wi * 32 + q;
+                sval[o] = w[wi * 32 + q];
+            }
             ++o;
         }
         base += tot;
@@ -137,18 +144,49 @@ __device__ int select_write(const int32_t* ccol, const double* cval, int C, int 
                 if ((k & msk) == pre) atomicAdd(&hist[(k >> shift) & 255], 1);
             }
             __syncthreads();
-            if (threadIdx.x == 0) {
-                int64_t nd = int64_t(s64[2]), cum = 0;
-                int d = 0;
-                for (d = 255; d >= 0; --d) {
-                    if (cum + hist[d] >= nd) break;
-                    cum += hist[d];
+            if (threadIdx.x < 32) {
+                // bins from the top: lane l covers bins 255-8l .. 248-8l; the bin where the running
+                // count reaches the number still needed holds the threshold
+                const int lane = threadIdx.x;
+                const int nd = int(s64[2]);
+                int loc[8], sum = 0;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    loc[j] = hist[255 - 8 * lane - j];
+                    sum += loc[j];
                 }
-                s64[0] = pre | (uint64_t(d) << shift);
-                s64[1] = msk | (uint64_t(255) << shift);
-                s64[2] = uint64_t(nd - cum);
+                int incl = sum;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(FULL, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                const unsigned bal = __ballot_sync(FULL, incl >= nd);
+                if (lane == __ffs(bal) - 1) {
+                    int cum = incl - sum, j = 0;
+                    for (; j < 7; ++j) {
+                        if (cum + loc[j] >= nd) break;
+                        cum += loc[j];
+                    }
+                    s64[0] = pre | (uint64_t(255 - 8 * lane - j) << shift);
+                    s64[1] = msk | (uint64_t(255) << shift);
+                    s64[2] = uint64_t(nd - cum);
+                    s64[3] = uint64_t(loc[j]);  // size of the threshold bin
+                }
             }
             __syncthreads();
+            if (s64[3] == 1 && shift > 0) {
+                // one element left in the threshold bin: it is the threshold, take its whole key
+                const uint64_t pre2 = s64[0], msk2 = s64[1];
+                for (int t = threadIdx.x; t < C; t += kThreads) {
+                    const uint64_t k = absbits(cval[t]);
+                    if ((k & msk2) == pre2) s64[4] = k;
+                }
+                __syncthreads();
+                if (threadIdx.x == 0) s64[0] = s64[4];
+                __syncthreads();
+                break;
+            }
         }
         T = s64[0];
         need = int(s64[2]);
@@ -178,7 +216,7 @@ __global__ void __launch_bounds__(kThreads) k_ilut(IlutDev d) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ int sh[kThreads / 32 + 1];
     __shared__ int hist[256];
-    __shared__ uint64_t s64[3];
+    __shared__ uint64_t s64[5];
     __shared__ int s_row, s_k, s_go, s_ulen;
     __shared__ double s_wk;
     uint32_t* pres = reinterpret_cast<uint32_t*>(smem);
@@ -187,6 +225,8 @@ __global__ void __launch_bounds__(kThreads) k_ilut(IlutDev d) {
                          : d.gw + size_t(blockIdx.x) * d.W;
     int32_t* ccol = d.gcand_col + size_t(blockIdx.x) * d.W;
     double* cval = d.gcand_val + size_t(blockIdx.x) * d.W;
+    __shared__ int32_t scol[kCandSh];
+    __shared__ double sval[kCandSh];
     const int b = d.b, M = d.M;
 
     for (int q = threadIdx.x; q < d.W; q += kThreads) w[q] = 0.0;
@@ -269,9 +309,10 @@ __global__ void __launch_bounds__(kThreads) k_ilut(IlutDev d) {
             if (threadIdx.x == 0) atomicMin(d.err_row, i);
             diag = 1.0;  // keep going so that no other CTA deadlocks; the host reports err_row
         }
-        int C = gather(w, pres, b + 1, d.W, true, tau_i, i - b, ccol, cval, sh);
+        int C = gather(w, pres, b + 1, d.W, true, tau_i, i - b, ccol, cval, scol, sval, sh);
         const size_t ub = size_t(i) * (M + 1);
-        int nu = select_write(ccol, cval, C, M, d.Ucol + ub + 1, d.Uval + ub + 1, sh, hist, s64);
+        int nu = select_write(C <= kCandSh ? scol : ccol, C <= kCandSh ? sval : cval, C, M, d.Ucol + ub + 1,
+                              d.Uval + ub + 1, sh, hist, s64);
         __threadfence();  // every writer orders its U entries before the release below
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -282,9 +323,10 @@ __global__ void __launch_bounds__(kThreads) k_ilut(IlutDev d) {
             st_release(d.done + i, 1);
         }
         // ---- L part: the kept multipliers
-        C = gather(w, pres, 0, b, false, 0.0, i - b, ccol, cval, sh);
+        C = gather(w, pres, 0, b, false, 0.0, i - b, ccol, cval, scol, sval, sh);
         const size_t lb = size_t(i) * M;
-        int nl = select_write(ccol, cval, C, M, d.Lcol + lb, d.Lval + lb, sh, hist, s64);
+        int nl = select_write(C <= kCandSh ? scol : ccol, C <= kCandSh ? sval : cval, C, M, d.Lcol + lb, d.Lval + lb,
+                              sh, hist, s64);
         if (threadIdx.x == 0) d.Llen[i] = nl;
         // ---- reset the window
         for (int wi = threadIdx.x; wi < d.nwords; wi += kThreads) {
@@ -369,7 +411,7 @@ int ilut_factorize_device(const DevCsr& A, int32_t band, double tau, double fill
     int max_smem = 0;
     PMG_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     const size_t bits_bytes = (size_t(2 * nwords) * 4 + 15) & ~size_t(15);
-    const size_t static_bytes = 4096;
+    const size_t static_bytes = 4096 + size_t(kCandSh) * 12;
     size_t dyn = bits_bytes + size_t(W) * 8;
     int smem_w = 1;
     if (dyn + static_bytes > size_t(max_smem)) {

@@ -381,15 +381,90 @@ static void scatter(HostCsr& A, const std::vector<int32_t>& rmap, const std::vec
         }
 }
 
+// ------------------------------------------------------------------ external values (F2)
+// 1D tables of the request (include/pmg_asm.h): a basis at the nel*nq Gauss abscissae followed
+// by x = 0 and x = 1, evaluated by the same basis_values_d1 calls the element loop makes.
+struct Table1D {
+    std::vector<double> B, dB;
+    std::vector<int32_t> first;
+    pmg_asm_table1d view{};
+    void build(const Knots& kv, const std::vector<double>& pts) {
+        const int p = kv.p;
+        B.assign(pts.size() * (p + 1), 0.0);
+        dB.assign(B.size(), 0.0);
+        first.resize(pts.size());
+        for (size_t i = 0; i < pts.size(); ++i) first[i] = basis_values_d1(kv, pts[i], &B[i * (p + 1)], &dB[i * (p + 1)]);
+        view = {p, int32_t(pts.size()), B.data(), dB.data(), first.data()};
+    }
+};
+
+static HostCsr external_values(const Domain& dom, const Space& rs, const Space& cs, const Cdr* c, int nq, int strip,
+                               pmg_asm_values_fn values) {
+    HostCsr A = make_pattern(dom, rs, cs);
+    const int nel = rs.nel;
+    Basis1D bs;
+    bs.build(rs.p, nel, nq);
+    std::vector<double> pts(bs.xq);
+    pts.push_back(0.0);
+    pts.push_back(1.0);
+    Table1D tr, tc;
+    tr.build(Knots::open_uniform(rs.p, nel), pts);
+    tc.build(Knots::open_uniform(cs.p, nel), pts);
+    const int np = int(dom.patches.size());
+    std::vector<Table1D> gx(np), gy(np);
+    std::vector<pmg_asm_patch> pv(np);
+    for (int P = 0; P < np; ++P) {
+        const NurbsPatch& g = dom.patches[P];
+        gx[P].build(g.gx, pts);
+        gy[P].build(g.gy, pts);
+        int mask = 0;
+        for (int e = 0; e < 4; ++e)
+            if (!dom.is_interface(P, e)) mask |= 1 << e;
+        pv[P] = {gx[P].view, gy[P].view, g.gx.nbasis(), g.cx.data(), g.cy.data(), g.w.data(),
+                 rs.l2g[P].data(), cs.l2g[P].data(), mask};
+    }
+    pmg_asm_request rq{};
+    rq.kind = c ? PMG_ASM_OPERATOR : PMG_ASM_MASS;
+    rq.nel = nel;
+    rq.nq = nq;
+    rq.npts = int32_t(pts.size());
+    rq.strip = strip;
+    rq.wq = bs.wq.data();
+    rq.row = tr.view;
+    rq.col = tc.view;
+    rq.n_patches = np;
+    rq.patches = pv.data();
+    if (c) {
+        for (int i = 0; i < 4; ++i) rq.D[i] = c->D[i / 2][i % 2];
+        rq.v[0] = c->v[0];
+        rq.v[1] = c->v[1];
+        rq.R = c->R;
+        rq.penalty = c->nitsche_scale * 4.0 * rs.p * rs.p * nel;
+    }
+    rq.nrows = A.nrows;
+    rq.ncols = A.ncols;
+    rq.rowptr = A.rowptr.data();
+    rq.col_idx = A.col.data();
+    rq.val = A.val.data();
+    const int rc = values(&rq);
+    if (rc == 1) throw GeometryError("nonpositive Jacobian determinant");
+    if (rc != 0) throw AssemblyError("external assembler failed (status " + std::to_string(rc) + ")");
+    return A;
+}
+
 // ------------------------------------------------------------------ assembly
 // a(u,v) = int (D grad u).grad v + (v.grad u) v + R u v  +  symmetric Nitsche on the
 // Dirichlet boundary:  - int (D grad u.n) v - int (D grad v.n) u + (eta/h) int u v,
 // eta = 4 p^2, h = 1/nel.  rhs = (f, v), plus the Nitsche
 // consistency terms -int (D grad v.n) g + (eta/h) int g v of inhomogeneous Dirichlet data g
 // (Benchmark 3).
-HostCsr assemble_operator(const Domain& dom, const Space& sp, const Cdr& c, std::vector<double>* rhs) {
-    HostCsr A = make_pattern(dom, sp, sp);
+HostCsr assemble_operator(const Domain& dom, const Space& sp, const Cdr& c, std::vector<double>* rhs,
+                          pmg_asm_values_fn values) {
     const int p = sp.p, nel = sp.nel, n1 = p + 1, n = nel + p, nq = p + 1;
+    // with an external producer of the values the loop below only forms the load vector
+    const bool ext = values != nullptr;
+    if (ext && !rhs) return external_values(dom, sp, sp, &c, nq, p + 1, values);
+    HostCsr A = ext ? external_values(dom, sp, sp, &c, nq, p + 1, values) : make_pattern(dom, sp, sp);
     Basis1D bs;
     bs.build(p, nel, nq);
     if (rhs) rhs->assign(sp.ndof, 0.0);
@@ -425,7 +500,7 @@ HostCsr assemble_operator(const Domain& dom, const Space& sp, const Cdr& c, std:
                     }
                 // stage 1: contract over the xi points
                 std::fill(S.begin(), S.end(), 0.0);
-                for (int b = 0; b < nq; ++b)
+                for (int b = 0; b < (ext ? 0 : nq); ++b)
                     for (int a = 0; a < nq; ++a) {
                         int q = a + b * nq;
                         const double *Bx = bs.b(ex, a), *dBx = bs.d(ex, a);
@@ -445,7 +520,7 @@ HostCsr assemble_operator(const Domain& dom, const Space& sp, const Cdr& c, std:
                     }
                 // stage 2: contract over the eta points
                 std::fill(E.begin(), E.end(), 0.0);
-                for (int b = 0; b < nq; ++b) {
+                for (int b = 0; b < (ext ? 0 : nq); ++b) {
                     const double *By = bs.b(ey, b), *dBy = bs.d(ey, b);
                     const double* Syy = &S[((0 * nq + b) * n1) * n1];
                     const double* Syd = &S[((1 * nq + b) * n1) * n1];
@@ -496,7 +571,7 @@ HostCsr assemble_operator(const Domain& dom, const Space& sp, const Cdr& c, std:
                                 flux[i + j * n1] = dg0 * nv[0] + dg1 * nv[1];
                             }
                         double w = ws * tl;
-                        for (int te = 0; te < nloc2; ++te)
+                        for (int te = 0; te < (ext ? 0 : nloc2); ++te)
                             for (int tr = 0; tr < nloc2; ++tr)
                                 E[size_t(te) * nloc2 + tr] += w * (-flux[tr] * phi[te] - flux[te] * phi[tr] + pen * phi[te] * phi[tr]);
                         if (rhs && c.g) {  // consistency terms of inhomogeneous data: -int (D grad v.n) g + (eta/h) int g v
@@ -505,7 +580,7 @@ HostCsr assemble_operator(const Domain& dom, const Space& sp, const Cdr& c, std:
                         }
                     }
                 }
-                scatter(A, l2g, l2g, n, n, ex, ey, n1, n1, E.data());
+                if (!ext) scatter(A, l2g, l2g, n, n, ex, ey, n1, n1, E.data());
                 if (rhs) {
                     for (int j1 = 0; j1 < n1; ++j1)
                         for (int i1 = 0; i1 < n1; ++i1) {
@@ -523,8 +598,9 @@ HostCsr assemble_operator(const Domain& dom, const Space& sp, const Cdr& c, std:
 
 // Mixed mass  P_ij = int phi_i^{(k)} phi_j^{(j)} dOmega over a common mesh; with the same
 // space on both sides this is the mass matrix M_k (eq. (24)).
-static HostCsr assemble_mixed_mass(const Domain& dom, const Space& rs, const Space& cs) {
+static HostCsr assemble_mixed_mass(const Domain& dom, const Space& rs, const Space& cs, pmg_asm_values_fn values) {
     if (rs.nel != cs.nel) throw AssemblyError("transfer: spaces on different meshes");
+    if (values) return external_values(dom, rs, cs, nullptr, std::max(rs.p, cs.p) + 1, std::max(rs.p, cs.p) + 1, values);
     HostCsr A = make_pattern(dom, rs, cs);
     const int nel = rs.nel, n1 = rs.p + 1, n2 = cs.p + 1, nq = std::max(rs.p, cs.p) + 1;
     const int nr = nel + rs.p, nc = nel + cs.p;
@@ -571,9 +647,11 @@ static HostCsr assemble_mixed_mass(const Domain& dom, const Space& rs, const Spa
     return A;
 }
 
-HostCsr assemble_mass(const Domain& dom, const Space& sp) { return assemble_mixed_mass(dom, sp, sp); }
-HostCsr assemble_transfer(const Domain& dom, const Space& fine_p, const Space& coarse_p) {
-    return assemble_mixed_mass(dom, fine_p, coarse_p);
+HostCsr assemble_mass(const Domain& dom, const Space& sp, pmg_asm_values_fn values) {
+    return assemble_mixed_mass(dom, sp, sp, values);
+}
+HostCsr assemble_transfer(const Domain& dom, const Space& fine_p, const Space& coarse_p, pmg_asm_values_fn values) {
+    return assemble_mixed_mass(dom, fine_p, coarse_p, values);
 }
 
 // Row-sum lumping M^L_ii = sum_j M_ij, ascending column order.
@@ -587,7 +665,9 @@ std::vector<double> lump(const HostCsr& M) {
     }
     return d;
 }
-std::vector<double> lumped_mass(const Domain& dom, const Space& sp) { return lump(assemble_mass(dom, sp)); }
+std::vector<double> lumped_mass(const Domain& dom, const Space& sp, pmg_asm_values_fn values) {
+    return lump(assemble_mass(dom, sp, values));
+}
 
 // p = 1 knot insertion (coarse nel -> 2 nel): coarse hat J = fine hat 2J + (fine hats 2J+-1)/2,
 // i.e. linear interpolation of nodal coefficients.

@@ -19,6 +19,8 @@
 #include <string>
 #include <vector>
 
+#include "../../../include/pmg_asm.h"
+
 namespace iga {
 
 // ---- errors (conventions of proj/include/iga/types.hpp:23-42) ----
@@ -92,11 +94,17 @@ struct Space {
 // Assembly.  All routines are deterministic and independent of
 // the number of worker threads (element strips coloured so no two concurrent strips
 // touch the same row; colour-major accumulation order).
-HostCsr assemble_operator(const Domain& dom, const Space& sp, const Cdr& c, std::vector<double>* rhs);
-HostCsr assemble_mass(const Domain& dom, const Space& sp);
-std::vector<double> lumped_mass(const Domain& dom, const Space& sp);   // row sums of M, elementwise
+//
+// `values` (optional, F2): an external producer of the matrix values -- the GPU assembler
+// pmg_asm_values of libpmg_cuda.so (include/pmg_asm.h).  The host then builds only the integer
+// structure, the 1D tables and the load vector; the values must equal the host loop's bit for bit.
+HostCsr assemble_operator(const Domain& dom, const Space& sp, const Cdr& c, std::vector<double>* rhs,
+                          pmg_asm_values_fn values = nullptr);
+HostCsr assemble_mass(const Domain& dom, const Space& sp, pmg_asm_values_fn values = nullptr);
+std::vector<double> lumped_mass(const Domain& dom, const Space& sp, pmg_asm_values_fn values = nullptr);  // row sums of M
 std::vector<double> lump(const HostCsr& M);                            // row sums of an assembled M
-HostCsr assemble_transfer(const Domain& dom, const Space& fine_p, const Space& coarse_p);  // P^k_j
+HostCsr assemble_transfer(const Domain& dom, const Space& fine_p, const Space& coarse_p,
+                          pmg_asm_values_fn values = nullptr);  // P^k_j
 HostCsr hrefine_p1(const Domain& dom, const Space& fine, const Space& coarse);  // knot insertion, p=1
 HostCsr transpose(const HostCsr& A);
 

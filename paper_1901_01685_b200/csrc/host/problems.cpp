@@ -109,7 +109,7 @@ static Cdr make_coeffs(int rhs_kind, const double* D, const double* v, double R)
     return c;
 }
 
-static Problem build_problem(const iga_problem_spec& s) {
+static Problem build_problem(const iga_problem_spec& s, pmg_asm_values_fn values = nullptr) {
     if (s.n_degrees < 1 || s.n_degrees > 8) throw ConfigError("degree list length");
     if (s.degrees[s.n_degrees - 1] != 1) throw ConfigError("degree list must end at 1");
     for (int i = 1; i < s.n_degrees; ++i)
@@ -130,10 +130,10 @@ static Problem build_problem(const iga_problem_spec& s) {
     for (int l = 0; l < s.n_degrees; ++l) {
         PLevel& L = pb.plev[l];
         L.degree = s.degrees[l];
-        L.A = assemble_operator(dom, spaces[l], l == 0 ? c : c_nof, l == 0 ? &pb.f : nullptr);
-        L.ML = lumped_mass(dom, spaces[l]);
+        L.A = assemble_operator(dom, spaces[l], l == 0 ? c : c_nof, l == 0 ? &pb.f : nullptr, values);
+        L.ML = lumped_mass(dom, spaces[l], values);
         if (l + 1 < s.n_degrees) {
-            L.P = assemble_transfer(dom, spaces[l], spaces[l + 1]);
+            L.P = assemble_transfer(dom, spaces[l], spaces[l + 1], values);
             L.PT = transpose(L.P);
         }
     }
@@ -142,7 +142,7 @@ static Problem build_problem(const iga_problem_spec& s) {
     Space fine = spaces.back();
     for (size_t j = 1; j < pb.hlev.size(); ++j) {
         Space coarse = Space::build(dom, 1, nel >> j);
-        pb.hlev[j].A = assemble_operator(dom, coarse, c_nof, nullptr);
+        pb.hlev[j].A = assemble_operator(dom, coarse, c_nof, nullptr, values);
         pb.hlev[j - 1].P = hrefine_p1(dom, fine, coarse);
         pb.hlev[j - 1].PT = transpose(pb.hlev[j - 1].P);
         fine = coarse;
@@ -213,10 +213,12 @@ int iga_config_spec(int config, int degree, iga_problem_spec* s) {
     return 0;
 }
 
-int iga_problem_build(const iga_problem_spec* s, iga_problem** out) {
+int iga_problem_build(const iga_problem_spec* s, iga_problem** out) { return iga_problem_build_with(s, nullptr, out); }
+
+int iga_problem_build_with(const iga_problem_spec* s, pmg_asm_values_fn values, iga_problem** out) {
     try {
         auto* h = new iga_problem_s;
-        h->pb = build_problem(*s);
+        h->pb = build_problem(*s, values);
         *out = h;
         return 0;
     } catch (const std::exception& e) {
@@ -297,6 +299,11 @@ int iga_problem_vec_copy(const iga_problem* h, int kind, int l, double* out) {
 // optional load in vec F), 1 = mass M, 2 = transfer P^{p}_{p2}, 3 = lumped mass (vec ML).
 int iga_matrix_build(int kind, int geometry, int p, int p2, int nel, const double* D, const double* v, double R,
                      double nitsche_scale, iga_problem** out) {
+    return iga_matrix_build_with(kind, geometry, p, p2, nel, D, v, R, nitsche_scale, nullptr, out);
+}
+
+int iga_matrix_build_with(int kind, int geometry, int p, int p2, int nel, const double* D, const double* v, double R,
+                          double nitsche_scale, pmg_asm_values_fn values, iga_problem** out) {
     try {
         Domain dom = make_domain(geometry, IGA_NUMBER_PATCH);
         Space sp = Space::build(dom, p, nel);
@@ -310,13 +317,13 @@ int iga_matrix_build(int kind, int geometry, int p, int p2, int nel, const doubl
             if (v) std::memcpy(vv, v, sizeof(vv));
             Cdr c = make_coeffs(IGA_RHS_ONE, Dd, vv, R);
             c.nitsche_scale = nitsche_scale > 0 ? nitsche_scale : 1.0;
-            L.A = assemble_operator(dom, sp, c, &h->pb.f);
+            L.A = assemble_operator(dom, sp, c, &h->pb.f, values);
         } else if (kind == 1) {
-            L.A = assemble_mass(dom, sp);
+            L.A = assemble_mass(dom, sp, values);
         } else if (kind == 2) {
-            L.A = assemble_transfer(dom, sp, Space::build(dom, p2, nel));
+            L.A = assemble_transfer(dom, sp, Space::build(dom, p2, nel), values);
         } else if (kind == 3) {
-            L.A = assemble_mass(dom, sp);
+            L.A = assemble_mass(dom, sp, values);
             L.ML = lump(L.A);
         } else {
             delete h;

@@ -1,8 +1,10 @@
-"""Problem / hierarchy inputs (host assembly through ``libiga_host.so``).
+"""Problem / hierarchy inputs (``libiga_host.so``; matrix values optionally from the GPU).
 
-The BASELINE.json configs 1-5 and the paper's Benchmarks 1-2.
+The BASELINE.json configs 1-5 and the paper's Benchmarks 1-3.
 Assembly is setup, not the solve path; it produces the FP64 CSR
-operators both the CUDA path and the CPU oracle consume.
+operators both the CUDA path and the CPU oracle consume.  ``assembly="gpu"`` (F2,
+SPEC.md:132-167) has ``libpmg_cuda.so``'s ``pmg_asm_values`` produce the values of every A_k,
+M_k and P^k_j; the result equals the host element loop bit for bit.
 """
 from __future__ import annotations
 
@@ -34,6 +36,8 @@ def _host():
     if not getattr(lib, "_typed", False):
         lib.iga_last_error.restype = ctypes.c_char_p
         lib.iga_problem_build.argtypes = [ctypes.POINTER(ProblemSpec), ctypes.POINTER(ctypes.c_void_p)]
+        lib.iga_problem_build_with.argtypes = [ctypes.POINTER(ProblemSpec), ctypes.c_void_p,
+                                               ctypes.POINTER(ctypes.c_void_p)]
         lib.iga_problem_free.argtypes = [ctypes.c_void_p]
         for fn in ("iga_problem_num_plevels", "iga_problem_num_hlevels"):
             getattr(lib, fn).argtypes = [ctypes.c_void_p]
@@ -54,6 +58,9 @@ def _host():
         lib.iga_matrix_build.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                          ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double, ctypes.c_double,
                                          ctypes.POINTER(ctypes.c_void_p)]
+        lib.iga_matrix_build_with.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                              ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double, ctypes.c_double,
+                                              ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)]
         lib._typed = True
     return lib
 
@@ -61,6 +68,17 @@ def _host():
 def _check(rc):
     if rc != 0:
         raise RuntimeError(_host().iga_last_error().decode())
+
+
+def values_hook(assembly):
+    """The ``pmg_asm_values_fn`` (include/pmg_asm.h) that produces matrix values: None / "host" =
+    the host element loop, "gpu" = ``pmg_asm_values`` of libpmg_cuda.so (no fallback: a missing
+    library or device raises), or a ctypes function pointer (tests)."""
+    if assembly is None or assembly == "host":
+        return None
+    if assembly == "gpu":
+        return ctypes.cast(load("libpmg_cuda.so").pmg_asm_values, ctypes.c_void_p)
+    return ctypes.cast(assembly, ctypes.c_void_p)
 
 
 @dataclass
@@ -159,14 +177,15 @@ def _vec(lib, h, kind, l) -> np.ndarray:
     return out
 
 
-def build(spec: ProblemSpec | int, degree: int = 0, name: str | None = None) -> Problem:
-    """Assemble a problem: ``spec`` is a ProblemSpec or a BASELINE config number 1..5."""
+def build(spec: ProblemSpec | int, degree: int = 0, name: str | None = None, assembly=None) -> Problem:
+    """Assemble a problem: ``spec`` is a ProblemSpec or a BASELINE config number 1..5;
+    ``assembly`` selects who produces the matrix values (see ``values_hook``)."""
     if isinstance(spec, int):
         name = name or (f"config{spec}" + (f"_p{degree}" if spec == 2 else ""))
         spec = config_spec(spec, degree)
     lib = _host()
     h = ctypes.c_void_p()
-    _check(lib.iga_problem_build(ctypes.byref(spec), ctypes.byref(h)))
+    _check(lib.iga_problem_build_with(ctypes.byref(spec), values_hook(assembly), ctypes.byref(h)))
     try:
         npl = lib.iga_problem_num_plevels(h)
         nhl = lib.iga_problem_num_hlevels(h)
@@ -195,7 +214,7 @@ def build(spec: ProblemSpec | int, degree: int = 0, name: str | None = None) -> 
 
 
 def matrix(kind: str, geometry: str = "square", p: int = 1, nel: int = 1, p2: int = 1, D=(1, 0, 0, 1), v=(0, 0),
-           R: float = 0.0, nitsche_scale: float = 0.0):
+           R: float = 0.0, nitsche_scale: float = 0.0, assembly=None):
     """One assembled operator: kind in {"A", "M", "P", "ML"}.
     Returns a Csr (and, for "A", the load vector f = (1, v); for "ML", the lumped mass)."""
     lib = _host()
@@ -203,7 +222,8 @@ def matrix(kind: str, geometry: str = "square", p: int = 1, nel: int = 1, p2: in
     Dv = np.ascontiguousarray(D, np.float64)
     vv = np.ascontiguousarray(v, np.float64)
     h = ctypes.c_void_p()
-    _check(lib.iga_matrix_build(k, GEOM[geometry], p, p2, nel, ptr(Dv), ptr(vv), R, nitsche_scale, ctypes.byref(h)))
+    _check(lib.iga_matrix_build_with(k, GEOM[geometry], p, p2, nel, ptr(Dv), ptr(vv), R, nitsche_scale,
+                                     values_hook(assembly), ctypes.byref(h)))
     try:
         M = _csr(lib, h, MAT_A, 0)
         if kind == "A":
