@@ -66,6 +66,9 @@ int iga_problem_degree(const iga_problem* h, int plevel);
  * P of p-level l maps level l+1 -> l; HP of h-level j maps level j+1 -> j. */
 int iga_problem_csr_shape(const iga_problem* h, int kind, int l, int32_t* nrows, int32_t* ncols, int64_t* nnz);
 int iga_problem_csr_copy(const iga_problem* h, int kind, int l, int32_t* rowptr, int32_t* col, double* val);
+/* borrowed pointers into the problem (valid until iga_problem_free): int64 offsets, columns, values */
+int iga_problem_csr_arrays(const iga_problem* h, int kind, int l, const int64_t** rowptr, const int32_t** col,
+                           const double** val);
 int iga_problem_vec_len(const iga_problem* h, int kind, int l);
 int iga_problem_vec_copy(const iga_problem* h, int kind, int l, double* out);
 

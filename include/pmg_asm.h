@@ -60,7 +60,9 @@ typedef struct pmg_asm_request {
     int32_t nrows, ncols;
     const int64_t* rowptr;   /* sparsity pattern (sorted unique columns) */
     const int32_t* col_idx;
-    double* val;             /* out: rowptr[nrows] values (host memory) */
+    double* val;             /* out: rowptr[nrows] values (host memory); NULL = not wanted */
+    double* lumped;          /* out: nrows row sums, entries added in ascending column order
+                                (lump_mass); NULL = not wanted */
 } pmg_asm_request;
 
 /* returns 0, or nonzero: 1 = nonpositive Jacobian determinant (geometry error), 2 = entry

@@ -244,4 +244,11 @@ PMG_HD bool gather_entry(const Params& P, const double* E, int e0, int ix, int i
     return true;
 }
 
+// ---- lump_mass: row sum in ascending column order (host `lump`)
+PMG_HD double row_sum(const double* val, int64_t kb, int64_t ke) {
+    double s = 0.0;
+    for (int64_t k = kb; k < ke; ++k) s += val[k];
+    return s;
+}
+
 }  // namespace pmgasm

@@ -13,6 +13,9 @@
 //                    element-matrix entry is written once and read once.
 // The arithmetic lives in asm_core.cuh.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -84,6 +87,12 @@ __global__ void __launch_bounds__(256) k_asm_gather(Params P, int e0, int r0, in
     }
 }
 
+__global__ void k_asm_rowsum(int32_t n, const int64_t* __restrict__ rowptr, const double* __restrict__ val,
+                             double* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = row_sum(val, rowptr[i], rowptr[i + 1]);
+}
+
 __global__ void k_asm_fill(int32_t* a, int64_t n, int32_t v) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i < n) a[i] = v;
@@ -121,7 +130,7 @@ struct DevTab {
 
 void check_request(const pmg_asm_request* rq) {
     auto bad = [](const char* m) { throw std::invalid_argument(std::string("pmg_asm_values: ") + m); };
-    if (!rq || !rq->patches || !rq->rowptr || !rq->col_idx || !rq->val || !rq->wq) bad("null pointer");
+    if (!rq || !rq->patches || !rq->rowptr || !rq->col_idx || (!rq->val && !rq->lumped) || !rq->wq) bad("null pointer");
     if (rq->kind != PMG_ASM_OPERATOR && rq->kind != PMG_ASM_MASS) bad("unknown kind");
     if (rq->row.p < 1 || rq->row.p > kMaxP || rq->col.p < 1 || rq->col.p > kMaxP) bad("degree outside 1..5");
     if (rq->kind == PMG_ASM_OPERATOR && rq->row.p != rq->col.p) bad("operator needs equal row and column spaces");
@@ -137,6 +146,16 @@ void check_request(const pmg_asm_request* rq) {
 
 int asm_values(const pmg_asm_request* rq) {
     check_request(rq);
+    const bool verbose = std::getenv("PMG_VERBOSE") != nullptr;
+    auto t_last = std::chrono::steady_clock::now();
+    double t_up = 0, t_kern = 0, t_down = 0;
+    auto lap = [&](double& acc) {
+        if (!verbose) return;
+        cudaDeviceSynchronize();
+        auto t = std::chrono::steady_clock::now();
+        acc += std::chrono::duration<double>(t - t_last).count();
+        t_last = t;
+    };
     const int nel = rq->nel, n1 = rq->row.p + 1, n2 = rq->col.p + 1;
     const int nr = nel + rq->row.p, nc = nel + rq->col.p;
     const int64_t nnz = rq->rowptr[rq->nrows];
@@ -159,6 +178,7 @@ int asm_values(const pmg_asm_request* rq) {
     d_bad.alloc(sizeof(int));
     PMG_CUDA(cudaMemset(d_bad.p, 0, sizeof(int)));
     d_g2l.alloc(size_t(rq->ncols) * sizeof(int32_t));
+    lap(t_up);
 
     // chunk of DOF rows whose element matrices fit the buffer (default 2 GiB; PMG_ASM_CHUNK_MB)
     static const int chunk_mb = env_int("PMG_ASM_CHUNK_MB", 2048);
@@ -180,6 +200,7 @@ int asm_values(const pmg_asm_request* rq) {
         P.dirichlet = g.dirichlet_edges;
         const int32_t* l2gr = d_l2gr.upload(g.l2g_row, size_t(nr) * nr);
         const int32_t* l2gc = d_l2gc.upload(g.l2g_col, size_t(nc) * nc);
+        lap(t_up);
         k_asm_fill<<<ceil_div(rq->ncols, 256), 256>>>(d_g2l.as<int32_t>(), rq->ncols, -1);
         k_asm_invert<<<ceil_div(int64_t(nc) * nc, 256), 256>>>(l2gc, nc * nc, d_g2l.as<int32_t>());
         PMG_LAUNCH_CHECK();
@@ -197,6 +218,7 @@ int asm_values(const pmg_asm_request* rq) {
             r0 = r1;
         }
         PMG_CUDA(cudaDeviceSynchronize());  // patch buffers are freed at the end of the iteration
+        lap(t_kern);
     }
     int bad = 0;
     PMG_CUDA(cudaMemcpy(&bad, d_bad.p, sizeof(int), cudaMemcpyDeviceToHost));
@@ -204,7 +226,18 @@ int asm_values(const pmg_asm_request* rq) {
         set_last_error("nonpositive Jacobian determinant");
         return 1;
     }
-    PMG_CUDA(cudaMemcpy(rq->val, d_val.p, size_t(nnz) * sizeof(double), cudaMemcpyDeviceToHost));
+    if (rq->val) PMG_CUDA(cudaMemcpy(rq->val, d_val.p, size_t(nnz) * sizeof(double), cudaMemcpyDeviceToHost));
+    if (rq->lumped) {
+        DevBuf d_sum;
+        d_sum.alloc(size_t(rq->nrows) * sizeof(double));
+        k_asm_rowsum<<<ceil_div(rq->nrows, 256), 256>>>(rq->nrows, rowptr, d_val.as<double>(), d_sum.as<double>());
+        PMG_LAUNCH_CHECK();
+        PMG_CUDA(cudaMemcpy(rq->lumped, d_sum.p, size_t(rq->nrows) * sizeof(double), cudaMemcpyDeviceToHost));
+    }
+    lap(t_down);
+    if (verbose)
+        fprintf(stderr, "[pmg] asm kind %d p %d/%d nel %d nnz %lld: upload %.3f s, kernels %.3f s, download %.3f s\n", rq->kind,
+                rq->row.p, rq->col.p, nel, (long long)nnz, t_up, t_kern, t_down);
     return 0;
 }
 

@@ -277,31 +277,42 @@ static HostCsr make_pattern(const Domain& dom, const Space& rs, const Space& cs)
     A.nrows = rs.ndof;
     A.ncols = cs.ndof;
     A.rowptr.assign(rs.ndof + 1, 0);
-    std::vector<std::vector<int32_t>> rows(rs.ndof);
-    parallel_for((rs.ndof + 1023) / 1024, [&](int64_t blk) {
+    // columns of row g, ascending and unique, into v
+    auto row_cols = [&](int32_t g, std::vector<int32_t>& v) {
+        v.clear();
+        const bool multi = cnt[g + 1] - cnt[g] > 1;
+        for (int o = cnt[g]; o < cnt[g + 1]; ++o) {
+            int P = occ[o] / rs.nloc, loc = occ[o] % rs.nloc;
+            int ix = loc % nr, iy = loc / nr;
+            const int32_t* map = cs.l2g[P].data();
+            for (int jy = std::max(0, iy - lo); jy <= std::min(nc - 1, iy + hi); ++jy)
+                for (int jx = std::max(0, ix - lo); jx <= std::min(nc - 1, ix + hi); ++jx) v.push_back(map[jx + jy * nc]);
+        }
+        if (multi || np > 1) {
+            std::sort(v.begin(), v.end());
+            v.erase(std::unique(v.begin(), v.end()), v.end());
+        }
+    };
+    // two passes over blocks of rows (lengths, then columns): no per-row allocations
+    const int64_t nblk = (rs.ndof + 1023) / 1024;
+    parallel_for(nblk, [&](int64_t blk) {
+        std::vector<int32_t> v;
         int32_t r0 = int32_t(blk * 1024), r1 = std::min<int32_t>(rs.ndof, r0 + 1024);
         for (int32_t g = r0; g < r1; ++g) {
-            auto& v = rows[g];
-            bool multi = cnt[g + 1] - cnt[g] > 1;
-            for (int o = cnt[g]; o < cnt[g + 1]; ++o) {
-                int P = occ[o] / rs.nloc, loc = occ[o] % rs.nloc;
-                int ix = loc % nr, iy = loc / nr;
-                for (int jy = std::max(0, iy - lo); jy <= std::min(nc - 1, iy + hi); ++jy)
-                    for (int jx = std::max(0, ix - lo); jx <= std::min(nc - 1, ix + hi); ++jx)
-                        v.push_back(cs.l2g[P][jx + jy * nc]);
-            }
-            if (multi || np > 1) {
-                std::sort(v.begin(), v.end());
-                v.erase(std::unique(v.begin(), v.end()), v.end());
-            }
+            row_cols(g, v);
+            A.rowptr[g + 1] = int64_t(v.size());
         }
     });
-    for (int32_t g = 0; g < rs.ndof; ++g) A.rowptr[g + 1] = A.rowptr[g] + int64_t(rows[g].size());
+    for (int32_t g = 0; g < rs.ndof; ++g) A.rowptr[g + 1] += A.rowptr[g];
     A.col.resize(A.rowptr.back());
-    A.val.assign(A.rowptr.back(), 0.0);
-    parallel_for(rs.ndof, [&](int64_t g) {
-        std::copy(rows[g].begin(), rows[g].end(), A.col.begin() + A.rowptr[g]);
-        std::vector<int32_t>().swap(rows[g]);
+    A.val.resize(A.rowptr.back());
+    parallel_for(nblk, [&](int64_t blk) {
+        std::vector<int32_t> v;
+        int32_t r0 = int32_t(blk * 1024), r1 = std::min<int32_t>(rs.ndof, r0 + 1024);
+        for (int32_t g = r0; g < r1; ++g) {
+            row_cols(g, v);
+            std::copy(v.begin(), v.end(), A.col.begin() + A.rowptr[g]);
+        }
     });
     return A;
 }
@@ -398,9 +409,42 @@ struct Table1D {
     }
 };
 
+// NurbsPatch::map with the geometry bases read from tables (the same basis_values_d1 results,
+// the same loop: identical X and J)
+static void tab_map(const NurbsPatch& g, const Table1D& tx, const Table1D& ty, int ptx, int pty, double X[2], double J[2][2]) {
+    const int px = g.gx.p, py = g.gy.p, nx = g.gx.nbasis();
+    const double *Nx = &tx.B[size_t(ptx) * (px + 1)], *dNx = &tx.dB[size_t(ptx) * (px + 1)];
+    const double *Ny = &ty.B[size_t(pty) * (py + 1)], *dNy = &ty.dB[size_t(pty) * (py + 1)];
+    const int fx = tx.first[ptx], fy = ty.first[pty];
+    double W = 0, Wx = 0, Wy = 0, S[2] = {0, 0}, Sx[2] = {0, 0}, Sy[2] = {0, 0};
+    for (int b = 0; b <= py; ++b)
+        for (int a = 0; a <= px; ++a) {
+            int k = (fx + a) + (fy + b) * nx;
+            double wk = g.w[k];
+            double v = Nx[a] * Ny[b] * wk, vx = dNx[a] * Ny[b] * wk, vy = Nx[a] * dNy[b] * wk;
+            W += v; Wx += vx; Wy += vy;
+            S[0] += v * g.cx[k]; S[1] += v * g.cy[k];
+            Sx[0] += vx * g.cx[k]; Sx[1] += vx * g.cy[k];
+            Sy[0] += vy * g.cx[k]; Sy[1] += vy * g.cy[k];
+        }
+    for (int r = 0; r < 2; ++r) {
+        X[r] = S[r] / W;
+        J[r][0] = (Sx[r] - X[r] * Wx) / W;
+        J[r][1] = (Sy[r] - X[r] * Wy) / W;
+    }
+}
+
+// `pattern` (optional): an operator with the sparsity pattern of the request (M_k has A_k's);
+// with `lumped` only the row sums are produced and the returned matrix is empty.
 static HostCsr external_values(const Domain& dom, const Space& rs, const Space& cs, const Cdr* c, int nq, int strip,
-                               pmg_asm_values_fn values) {
-    HostCsr A = make_pattern(dom, rs, cs);
+                               pmg_asm_values_fn values, const HostCsr* pattern = nullptr,
+                               std::vector<double>* lumped = nullptr) {
+    HostCsr A;
+    if (!pattern) {
+        A = make_pattern(dom, rs, cs);
+        pattern = &A;
+    }
+    if (lumped) lumped->assign(pattern->nrows, 0.0);
     const int nel = rs.nel;
     Basis1D bs;
     bs.build(rs.p, nel, nq);
@@ -441,11 +485,12 @@ static HostCsr external_values(const Domain& dom, const Space& rs, const Space& 
         rq.R = c->R;
         rq.penalty = c->nitsche_scale * 4.0 * rs.p * rs.p * nel;
     }
-    rq.nrows = A.nrows;
-    rq.ncols = A.ncols;
-    rq.rowptr = A.rowptr.data();
-    rq.col_idx = A.col.data();
-    rq.val = A.val.data();
+    rq.nrows = pattern->nrows;
+    rq.ncols = pattern->ncols;
+    rq.rowptr = pattern->rowptr.data();
+    rq.col_idx = pattern->col.data();
+    rq.val = pattern == &A ? A.val.data() : nullptr;
+    rq.lumped = lumped ? lumped->data() : nullptr;
     const int rc = values(&rq);
     if (rc == 1) throw GeometryError("nonpositive Jacobian determinant");
     if (rc != 0) throw AssemblyError("external assembler failed (status " + std::to_string(rc) + ")");
@@ -473,6 +518,11 @@ HostCsr assemble_operator(const Domain& dom, const Space& sp, const Cdr& c, std:
     for (size_t P = 0; P < dom.patches.size(); ++P) {
         const NurbsPatch& geo = dom.patches[P];
         const auto& l2g = sp.l2g[P];
+        Table1D tgx, tgy;  // geometry bases at the abscissae (load-vector-only pass)
+        if (ext) {
+            tgx.build(geo.gx, bs.xq);
+            tgy.build(geo.gy, bs.xq);
+        }
         for_each_element_strip(nel, p + 1, [&](int ey) {
             std::vector<double> E(size_t(nloc2) * nloc2), S(4 * size_t(nq) * n1 * n1);
             std::vector<double> K(4 * nq * nq), C(2 * nq * nq), Mr(nq * nq), Fq(nq * nq), Fb(nloc2);
@@ -481,11 +531,16 @@ HostCsr assemble_operator(const Domain& dom, const Space& sp, const Cdr& c, std:
                 for (int b = 0; b < nq; ++b)
                     for (int a = 0; a < nq; ++a) {
                         double X[2], J[2][2], G[2][2], det;
-                        geo.map(bs.xq[ex * nq + a], bs.xq[ey * nq + b], X, J);
+                        if (ext) tab_map(geo, tgx, tgy, ex * nq + a, ey * nq + b, X, J);
+                        else geo.map(bs.xq[ex * nq + a], bs.xq[ey * nq + b], X, J);
                         inv2(J, G, det);
                         if (!(det > 0)) throw GeometryError("nonpositive Jacobian determinant");
                         double w = bs.wq[ex * nq + a] * bs.wq[ey * nq + b] * det;
                         int q = a + b * nq;
+                        if (ext) {  // only the load vector is formed here
+                            Fq[q] = c.f ? w * c.f(X[0], X[1]) : 0.0;
+                            continue;
+                        }
                         // K = w G D G^T (parametric diffusion tensor)
                         for (int r = 0; r < 2; ++r)
                             for (int s = 0; s < 2; ++s) {
@@ -665,8 +720,14 @@ std::vector<double> lump(const HostCsr& M) {
     }
     return d;
 }
-std::vector<double> lumped_mass(const Domain& dom, const Space& sp, pmg_asm_values_fn values) {
-    return lump(assemble_mass(dom, sp, values));
+std::vector<double> lumped_mass(const Domain& dom, const Space& sp, pmg_asm_values_fn values, const HostCsr* pattern) {
+    if (!values) return lump(assemble_mass(dom, sp));
+    // external producer: M_k's values stay with it, only the row sums come back
+    std::vector<double> d;
+    external_values(dom, sp, sp, nullptr, sp.p + 1, sp.p + 1, values, pattern, &d);
+    for (double s : d)
+        if (!(s > 0)) throw AssemblyError("lump_mass: nonpositive row sum");
+    return d;
 }
 
 // p = 1 knot insertion (coarse nel -> 2 nel): coarse hat J = fine hat 2J + (fine hats 2J+-1)/2,
@@ -703,23 +764,55 @@ HostCsr hrefine_p1(const Domain& dom, const Space& fine, const Space& coarse) {
     return Q;
 }
 
-// CSR transpose; rows of the result list entries in ascending original-row order.
+// CSR transpose; rows of the result list entries in ascending original-row order.  Output rows
+// are independent: counts by one pass, then every block of output rows scatters its own entries
+// (threads scan disjoint row ranges of A and keep the entries that fall into their column block
+// -- done per block through a column-bucketed index so A is read once per pass).
 HostCsr transpose(const HostCsr& A) {
     HostCsr T;
     T.nrows = A.ncols;
     T.ncols = A.nrows;
     T.rowptr.assign(size_t(A.ncols) + 1, 0);
-    for (int64_t k = 0; k < A.nnz(); ++k) T.rowptr[A.col[k] + 1]++;
-    for (int32_t i = 0; i < A.ncols; ++i) T.rowptr[i + 1] += T.rowptr[i];
+    const int nt = std::max(1, num_threads());
+    // pass 1: per-thread column counts over contiguous row ranges of A
+    const int64_t nchunk = nt;
+    std::vector<std::vector<int32_t>> cnt(nchunk);
+    auto range = [&](int64_t c, int32_t& r0, int32_t& r1) {
+        r0 = int32_t(int64_t(A.nrows) * c / nchunk);
+        r1 = int32_t(int64_t(A.nrows) * (c + 1) / nchunk);
+    };
+    parallel_for(nchunk, [&](int64_t c) {
+        int32_t r0, r1;
+        range(c, r0, r1);
+        auto& v = cnt[c];
+        v.assign(size_t(A.ncols), 0);
+        for (int64_t k = A.rowptr[r0]; k < A.rowptr[r1]; ++k) v[A.col[k]]++;
+    });
+    // offsets: column j's entries of chunk c start at rowptr[j] + sum_{c' < c} cnt[c'][j]
+    for (int32_t j = 0; j < A.ncols; ++j) {
+        int64_t tot = 0;
+        for (int64_t c = 0; c < nchunk; ++c) {
+            int32_t t = cnt[c][j];
+            cnt[c][j] = int32_t(tot);
+            tot += t;
+        }
+        T.rowptr[j + 1] = T.rowptr[j] + tot;
+    }
     T.col.resize(A.nnz());
     T.val.resize(A.nnz());
-    std::vector<int64_t> pos(T.rowptr.begin(), T.rowptr.end() - 1);
-    for (int32_t i = 0; i < A.nrows; ++i)
-        for (int64_t k = A.rowptr[i]; k < A.rowptr[i + 1]; ++k) {
-            int64_t o = pos[A.col[k]]++;
-            T.col[o] = i;
-            T.val[o] = A.val[k];
-        }
+    // pass 2: every chunk scatters its rows (ascending) into its own slots: ascending original rows
+    parallel_for(nchunk, [&](int64_t c) {
+        int32_t r0, r1;
+        range(c, r0, r1);
+        auto& pos = cnt[c];
+        for (int32_t i = r0; i < r1; ++i)
+            for (int64_t k = A.rowptr[i]; k < A.rowptr[i + 1]; ++k) {
+                const int32_t j = A.col[k];
+                const int64_t o = T.rowptr[j] + pos[j]++;
+                T.col[o] = i;
+                T.val[o] = A.val[k];
+            }
+    });
     return T;
 }
 

@@ -101,7 +101,10 @@ struct Space {
 HostCsr assemble_operator(const Domain& dom, const Space& sp, const Cdr& c, std::vector<double>* rhs,
                           pmg_asm_values_fn values = nullptr);
 HostCsr assemble_mass(const Domain& dom, const Space& sp, pmg_asm_values_fn values = nullptr);
-std::vector<double> lumped_mass(const Domain& dom, const Space& sp, pmg_asm_values_fn values = nullptr);  // row sums of M
+// row sums of M; `pattern` (optional, external values only): an operator on the same space, whose
+// sparsity pattern M shares
+std::vector<double> lumped_mass(const Domain& dom, const Space& sp, pmg_asm_values_fn values = nullptr,
+                                const HostCsr* pattern = nullptr);
 std::vector<double> lump(const HostCsr& M);                            // row sums of an assembled M
 HostCsr assemble_transfer(const Domain& dom, const Space& fine_p, const Space& coarse_p,
                           pmg_asm_values_fn values = nullptr);  // P^k_j

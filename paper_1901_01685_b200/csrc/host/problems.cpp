@@ -8,6 +8,9 @@
 // Exposed through the C ABI in include/iga_host.h.
 #include <cmath>
 #include <cstring>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <memory>
 
 #include "discretization.hpp"
@@ -116,6 +119,15 @@ static Problem build_problem(const iga_problem_spec& s, pmg_asm_values_fn values
         if (!(s.degrees[i] < s.degrees[i - 1])) throw ConfigError("degrees must be strictly decreasing");
     if (s.h_exp < 2 || s.h_exp > 12) throw ConfigError("h_exp out of range");
     if (s.coarsest_h_exp < 1 || s.coarsest_h_exp > s.h_exp) throw ConfigError("coarsest_h_exp out of range");
+    // IGA_VERBOSE: wall time of every phase on stderr
+    const bool verbose = std::getenv("IGA_VERBOSE") != nullptr;
+    auto t_last = std::chrono::steady_clock::now();
+    auto lap = [&](const char* what, int l) {
+        if (!verbose) return;
+        auto t = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[iga] %-22s level %d: %.3f s\n", what, l, std::chrono::duration<double>(t - t_last).count());
+        t_last = t;
+    };
     Domain dom = make_domain(s.geometry, s.numbering);
     Cdr c = make_coeffs(s.rhs, s.D, s.v, s.R);
     c.nitsche_scale = s.nitsche_scale > 0 ? s.nitsche_scale : 1.0;
@@ -131,10 +143,14 @@ static Problem build_problem(const iga_problem_spec& s, pmg_asm_values_fn values
         PLevel& L = pb.plev[l];
         L.degree = s.degrees[l];
         L.A = assemble_operator(dom, spaces[l], l == 0 ? c : c_nof, l == 0 ? &pb.f : nullptr, values);
-        L.ML = lumped_mass(dom, spaces[l], values);
+        lap("operator A_k (+ load)", l);
+        L.ML = lumped_mass(dom, spaces[l], values, &L.A);
+        lap("lumped mass", l);
         if (l + 1 < s.n_degrees) {
             L.P = assemble_transfer(dom, spaces[l], spaces[l + 1], values);
+            lap("transfer P", l);
             L.PT = transpose(L.P);
+            lap("transpose", l);
         }
     }
     // h-levels at p = 1: h, 2h, ... down to 2^-coarsest (rediscretised)
@@ -146,6 +162,7 @@ static Problem build_problem(const iga_problem_spec& s, pmg_asm_values_fn values
         pb.hlev[j - 1].P = hrefine_p1(dom, fine, coarse);
         pb.hlev[j - 1].PT = transpose(pb.hlev[j - 1].P);
         fine = coarse;
+        lap("h-level A, P, P^T", int(j));
     }
     const int32_t N = spaces[0].ndof;
     pb.u0.assign(N, 0.0);
@@ -269,6 +286,21 @@ int iga_problem_csr_copy(const iga_problem* h, int kind, int l, int32_t* rowptr,
         for (int32_t i = 0; i <= A->nrows; ++i) rowptr[i] = int32_t(A->rowptr[i]);
         std::memcpy(col, A->col.data(), A->col.size() * sizeof(int32_t));
         std::memcpy(val, A->val.data(), A->val.size() * sizeof(double));
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
+int iga_problem_csr_arrays(const iga_problem* h, int kind, int l, const int64_t** rowptr, const int32_t** col,
+                           const double** val) {
+    try {
+        const HostCsr* A = pick(h, kind, l);
+        if (!A) return -1;
+        *rowptr = A->rowptr.data();
+        *col = A->col.data();
+        *val = A->val.data();
         return 0;
     } catch (const std::exception& e) {
         g_err = e.what();

@@ -47,6 +47,7 @@ def _host():
                                               ctypes.POINTER(ctypes.c_int64)]
         lib.iga_problem_csr_copy.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                              ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+        lib.iga_problem_csr_arrays.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int] + [ctypes.POINTER(ctypes.c_void_p)] * 3
         lib.iga_problem_vec_len.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
         lib.iga_problem_vec_copy.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
         lib.iga_config_spec.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ProblemSpec)]
@@ -160,9 +161,36 @@ def set_threads(n: int) -> None:
     _host().iga_set_num_threads(n)
 
 
-def _csr(lib, h, kind, l) -> Csr:
+class _Owner:
+    """Keeps a host problem alive while numpy arrays view its memory."""
+
+    def __init__(self, lib, h):
+        self.lib, self.h = lib, h
+
+    def __del__(self):
+        if self.h:
+            self.lib.iga_problem_free(self.h)
+            self.h = None
+
+
+def _view(owner, address, ctype, n, dtype):
+    if n == 0:
+        return np.empty(0, dtype)
+    buf = (ctype * n).from_address(address)
+    buf._owner = owner  # the array's base chain reaches the owner
+    return np.frombuffer(buf, dtype=dtype)
+
+
+def _csr(lib, h, kind, l, owner=None) -> Csr:
     nr, nc, nnz = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int64()
     _check(lib.iga_problem_csr_shape(h, kind, l, ctypes.byref(nr), ctypes.byref(nc), ctypes.byref(nnz)))
+    if owner is not None and nnz.value <= np.iinfo(np.int32).max:
+        # zero-copy views of columns and values (the big arrays); offsets converted to int32
+        rp, ci, va = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+        _check(lib.iga_problem_csr_arrays(h, kind, l, ctypes.byref(rp), ctypes.byref(ci), ctypes.byref(va)))
+        rowptr = _view(owner, rp.value, ctypes.c_int64, nr.value + 1, np.int64).astype(np.int32)
+        return Csr(nr.value, nc.value, rowptr, _view(owner, ci.value, ctypes.c_int32, nnz.value, np.int32),
+                   _view(owner, va.value, ctypes.c_double, nnz.value, np.float64))
     rowptr = np.empty(nr.value + 1, np.int32)
     col = np.empty(nnz.value, np.int32)
     val = np.empty(nnz.value, np.float64)
@@ -186,28 +214,26 @@ def build(spec: ProblemSpec | int, degree: int = 0, name: str | None = None, ass
     lib = _host()
     h = ctypes.c_void_p()
     _check(lib.iga_problem_build_with(ctypes.byref(spec), values_hook(assembly), ctypes.byref(h)))
-    try:
-        npl = lib.iga_problem_num_plevels(h)
-        nhl = lib.iga_problem_num_hlevels(h)
-        pl = []
-        for l in range(npl):
-            lev = PLevel(lib.iga_problem_degree(h, l), _csr(lib, h, MAT_A, l), _vec(lib, h, VEC_ML, l))
-            if l + 1 < npl:
-                lev.P = _csr(lib, h, MAT_P, l)
-                lev.PT = _csr(lib, h, MAT_PT, l)
-            pl.append(lev)
-        hl = []
-        for j in range(nhl):
-            A = pl[-1].A if j == 0 else _csr(lib, h, MAT_HA, j)
-            lev = HLevel(A)
-            if j + 1 < nhl:
-                lev.P = _csr(lib, h, MAT_HP, j)
-                lev.PT = _csr(lib, h, MAT_HPT, j)
-            hl.append(lev)
-        f = _vec(lib, h, VEC_F, 0)
-        u0 = _vec(lib, h, VEC_U0, 0)
-    finally:
-        lib.iga_problem_free(h)
+    owner = _Owner(lib, h)  # frees the host problem once the last array viewing it is gone
+    npl = lib.iga_problem_num_plevels(h)
+    nhl = lib.iga_problem_num_hlevels(h)
+    pl = []
+    for l in range(npl):
+        lev = PLevel(lib.iga_problem_degree(h, l), _csr(lib, h, MAT_A, l, owner), _vec(lib, h, VEC_ML, l))
+        if l + 1 < npl:
+            lev.P = _csr(lib, h, MAT_P, l, owner)
+            lev.PT = _csr(lib, h, MAT_PT, l, owner)
+        pl.append(lev)
+    hl = []
+    for j in range(nhl):
+        A = pl[-1].A if j == 0 else _csr(lib, h, MAT_HA, j, owner)
+        lev = HLevel(A)
+        if j + 1 < nhl:
+            lev.P = _csr(lib, h, MAT_HP, j, owner)
+            lev.PT = _csr(lib, h, MAT_HPT, j, owner)
+        hl.append(lev)
+    f = _vec(lib, h, VEC_F, 0)
+    u0 = _vec(lib, h, VEC_U0, 0)
     sd = {k: (list(getattr(spec, k)) if k in ("D", "v", "degrees") else getattr(spec, k)) for k, _ in spec._fields_}
     sd["degrees"] = sd["degrees"][: spec.n_degrees]
     return Problem(name or "custom", sd, pl, hl, f, u0)

@@ -51,8 +51,27 @@ def launch_summary(csv_path, out_path, cmd):
     return agg
 
 
-def full_summary(rep, out_txt, out_json):
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+def full_summary(reps, out_txt, out_json):
+    """reps: list of (title, path); a path is an .ncu-rep (read with ncu -i) or a raw-page CSV
+    exported on the GPU box (scripts/profile_round2.sh)"""
+    traffic = collections.defaultdict(list)
+    with open(out_txt, "w") as fh:
+        fh.write("ncu --set full --clock-control none (raw page, demangled names); DRAM bytes and durations per launch\n")
+        for title, path in reps:
+            if not os.path.exists(path):
+                continue
+            fh.write(f"\n== {title} ({os.path.basename(path)})\n")
+            _one_report(path, fh, traffic)
+    json.dump({k: {"dram_bytes_per_launch": sum(v) / len(v), "launches_captured": len(v)} for k, v in traffic.items()},
+              open(out_json, "w"), indent=1)
+
+
+def _one_report(rep, fh, traffic):
+    if rep.endswith(".csv"):
+        raw = open(rep).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--print-kernel-base", "demangled"],
+                             capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
     want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
@@ -71,10 +90,7 @@ def full_summary(rep, out_txt, out_json):
                  "s": 1e3}.get(u, 1)
         return x * scale
 
-    traffic = collections.defaultdict(list)
-    with open(out_txt, "w") as fh:
-        fh.write("ncu --set full --clock-control none --import-source on (first launches of the sweep kernels / "
-                 "k_rowop in the timed region)\n")
+    if True:
         fh.write("kernel | duration ms | DRAM read MB | DRAM write MB | DRAM GB/s | L2 hit % | regs | grid x block\n")
         for r in rows[2:]:
             if len(r) != len(hdr):
@@ -84,13 +100,12 @@ def full_summary(rep, out_txt, out_json):
             rd = val(r, "dram__bytes_read.sum") or 0.0
             wr = val(r, "dram__bytes_write.sum") or 0.0
             gbs = (rd + wr) / (d * 1e-3) / 1e9 if d else 0.0
-            traffic[name].append(rd + wr)
-            fh.write(f"{name} | {d:.3f} | {rd / 1e6:.1f} | {wr / 1e6:.1f} | {gbs:.1f} | "
+            grid = int(val(r, 'launch__grid_size') or 0)
+            traffic[f"{name} grid {grid}"].append(rd + wr)
+            fh.write(f"{name} | {d:.4f} | {rd / 1e6:.1f} | {wr / 1e6:.1f} | {gbs:.1f} | "
                      f"{val(r, 'lts__t_sector_hit_rate.pct') or 0:.1f} | "
                      f"{int(val(r, 'launch__registers_per_thread') or 0)} | "
-                     f"{int(val(r, 'launch__grid_size') or 0)} x {int(val(r, 'launch__block_size') or 0)}\n")
-    json.dump({k: {"dram_bytes_per_launch": sum(v) / len(v), "launches_captured": len(v)} for k, v in traffic.items()},
-              open(out_json, "w"), indent=1)
+                     f"{grid} x {int(val(r, 'launch__block_size') or 0)}\n")
 
 
 def main():
@@ -100,8 +115,12 @@ def main():
           "solve)"
     launch_summary(os.path.join(src, "launches.csv"), os.path.join(dst, "launch_summary.txt"), cmd)
     shutil.copy(os.path.join(src, "launches.csv"), os.path.join(dst, "launches_config5_ilut_solve.csv"))
-    full_summary(os.path.join(src, "prof_full.ncu-rep"), os.path.join(dst, "ncu_full_summary.txt"),
-                 os.path.join(dst, "traffic.json"))
+    j = lambda f: os.path.join(src, f)
+    full = j("prof_full_raw.csv") if os.path.exists(j("prof_full_raw.csv")) else j("prof_full.ncu-rep")
+    full_summary([("config 5 ILUT solve: first launches of every kernel of one V-cycle", full),
+                  ("config 5 Gauss-Seidel solve: upper-sum pre-pass, GS sweep", j("gs_full_raw.csv")),
+                  ("setup on config 3: GPU assembly kernels, GPU ILUT", j("setup_full_raw.csv"))],
+                 os.path.join(dst, "ncu_full_summary.txt"), os.path.join(dst, "traffic.json"))
     if os.path.exists(os.path.join(src, "prof_plain.json")):
         shutil.copy(os.path.join(src, "prof_plain.json"), os.path.join(dst, "bench_line_under_profile_region.json"))
 

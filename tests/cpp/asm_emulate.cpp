@@ -23,7 +23,13 @@ extern "C" int asm_emulate_values(const pmg_asm_request* rq) {
     P.wq = rq->wq; P.row = tab(rq->row); P.col = tab(rq->col);
     std::memcpy(P.D, rq->D, sizeof(P.D));
     P.v[0] = rq->v[0]; P.v[1] = rq->v[1]; P.R = rq->R; P.pen = rq->penalty;
-    std::memset(rq->val, 0, size_t(nnz) * sizeof(double));
+    std::vector<double> own;
+    double* val = rq->val;
+    if (!val) {
+        own.resize(size_t(nnz));
+        val = own.data();
+    }
+    std::memset(val, 0, size_t(nnz) * sizeof(double));
     std::vector<double> E(size_t(nel) * nel * esz);
     std::vector<int32_t> g2l(rq->ncols);
     for (int p = 0; p < rq->n_patches; ++p) {
@@ -58,10 +64,12 @@ extern "C" int asm_emulate_values(const pmg_asm_request* rq) {
                 for (int64_t k = rq->rowptr[row]; k < rq->rowptr[row + 1]; ++k) {
                     const int32_t lc = g2l[rq->col_idx[k]];
                     if (lc < 0) continue;
-                    double acc = rq->val[k];
-                    if (gather_entry(P, E.data(), 0, ix, iy, lc % nc, lc / nc, acc)) rq->val[k] = acc;
+                    double acc = val[k];
+                    if (gather_entry(P, E.data(), 0, ix, iy, lc % nc, lc / nc, acc)) val[k] = acc;
                 }
             }
     }
+    if (rq->lumped)
+        for (int32_t i = 0; i < rq->nrows; ++i) rq->lumped[i] = row_sum(val, rq->rowptr[i], rq->rowptr[i + 1]);
     return 0;
 }
