@@ -98,6 +98,19 @@ bool env_flag(const char* name) {
 }
 bool force_levelsched() { return env_flag("PMG_FORCE_LEVELSCHED"); }
 
+// PMG_VERBOSE: wall time of setup phases on stderr
+struct Lap {
+    bool on = getenv("PMG_VERBOSE") != nullptr;
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    void operator()(const char* what, long long n = 0) {
+        if (!on) return;
+        cudaDeviceSynchronize();
+        auto now = std::chrono::steady_clock::now();
+        fprintf(stderr, "[pmg] setup %-28s n=%lld: %.3f s\n", what, n, std::chrono::duration<double>(now - t).count());
+        t = now;
+    }
+};
+
 struct Stream {
     cudaStream_t s = nullptr;
     Stream() { PMG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)); }
@@ -229,15 +242,20 @@ void gs_apply(pmg_csr_s* A, const double* f, const double* uo, double* un, doubl
 
 pmg_csr_s* make_csr(const pmg_csr_view& v, cudaStream_t st) {
     auto h = std::make_unique<pmg_csr_s>();
+    Lap lap;
     h->A = upload(v, st);
+    lap("csr upload", v.nrows);
     h->h_rowptr.assign(v.rowptr, v.rowptr + v.nrows + 1);
     h->h_col.assign(v.col, v.col + h->A.nnz);
     h->h_val.assign(v.val, v.val + h->A.nnz);
+    lap("csr host copy", v.nrows);
     h->band = pmg_host::bandwidth(v.nrows, v.rowptr, v.col);
     h->seg = force_levelsched() ? 0 : detect_segment(v.nrows, v.rowptr, v.col);
     if (!force_levelsched() && v.nrows == v.ncols) h->starts = detect_segment_starts(v.nrows, v.rowptr, v.col);
+    lap("csr band/segments", v.nrows);
     sell_build(h->S, v.nrows, h->A.rowptr, h->A.col, h->A.val, nullptr, kPickAll, nullptr, nullptr, st);
     PMG_CUDA(cudaStreamSynchronize(st));
+    lap("csr sell", v.nrows);
     return h.release();
 }
 
@@ -304,16 +322,27 @@ void ensure_gs(pmg_csr_s* h, cudaStream_t st) {
     h->gs_ready = true;
 }
 
-// ILUT of csr under `ordering`; on zero pivot returns PMG_ZERO_PIVOT with *err_row
-int make_factor(pmg_csr_s* A, double tau, double fillfactor, int ordering, pmg_factor_s** out, int64_t* err_row,
-                cudaStream_t st) {
+// ILUT of csr under `ordering` in two steps, so that the factorisations of a hierarchy's levels run
+// concurrently: factor_begin permutes (RCM) and launches the factorisation on `sj`; factor_end waits
+// for it and builds level sets, sweep layouts and plans on `st`.  On zero pivot factor_end returns
+// PMG_ZERO_PIVOT with *err_row.
+struct PendingFactor {
+    std::unique_ptr<pmg_factor_s> F;
+    pmg_csr_s* A = nullptr;
+    DevCsr owned;
+    IlutJob* job = nullptr;
+};
+
+PendingFactor factor_begin(pmg_csr_s* A, double tau, double fillfactor, int ordering, int max_ctas, cudaStream_t sj) {
     if (A->A.n != A->A.m) throw ArgError("ilut: matrix not square", PMG_ERR_DIM);
     if (!(tau >= 0) || !(fillfactor >= 1)) throw ArgError("ilut: tau >= 0 and fillfactor >= 1 required", PMG_ERR_ARG);
-    auto F = std::make_unique<pmg_factor_s>();
+    PendingFactor pf;
+    pf.A = A;
+    pf.F = std::make_unique<pmg_factor_s>();
+    auto& F = pf.F;
     const int32_t n = A->A.n;
     F->n = n;
     DevCsr Ap = A->A;
-    DevCsr owned;
     int32_t band = A->band;
     F->seg = A->seg;
     F->starts = A->starts;
@@ -325,17 +354,32 @@ int make_factor(pmg_csr_s* A, double tau, double fillfactor, int ordering, pmg_f
                                            bci, bv);
         pmg_csr_view v{n, n, brp.data(), bci.data(), bv.data()};
         F->seg = force_levelsched() ? 0 : detect_segment(n, brp.data(), bci.data());
-        owned = upload(v, st);
-        Ap = owned;
+        pf.owned = upload(v, sj);
+        Ap = pf.owned;
         F->perm = dalloc<int32_t>(n);
-        PMG_CUDA(cudaMemcpyAsync(F->perm, F->h_perm.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, st));
-        PMG_CUDA(cudaStreamSynchronize(st));
+        PMG_CUDA(cudaMemcpyAsync(F->perm, F->h_perm.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, sj));
+        PMG_CUDA(cudaStreamSynchronize(sj));
     } else if (ordering != PMG_ORDER_NONE) {
         throw ArgError("unknown ordering", PMG_ERR_ARG);
     }
-    int rc = ilut_factorize_device(Ap, band, tau, fillfactor, F->L, F->U, err_row, &F->seconds, st);
-    owned.free();
+    pf.job = ilut_launch(Ap, band, tau, fillfactor, max_ctas, sj);
+    return pf;
+}
+
+int factor_end(PendingFactor& pf, pmg_factor_s** out, int64_t* err_row, cudaStream_t st, cudaEvent_t ref = nullptr,
+               double* since_ref = nullptr) {
+    auto& F = pf.F;
+    pmg_csr_s* A = pf.A;
+    const int32_t n = F->n;
+    IlutJob* job = pf.job;
+    pf.job = nullptr;
+    int rc = ilut_finish(job, F->L, F->U, err_row, &F->seconds, ref, since_ref);
+    pf.owned.free();
+    if (getenv("PMG_VERBOSE"))
+        fprintf(stderr, "[pmg] ilut n=%d band=%d nnz(A)=%lld: %.3f s (%.2f us/row)\n", n, A->band, (long long)A->A.nnz,
+                F->seconds, 1e6 * F->seconds / std::max(n, 1));
     if (rc != 0) return PMG_ZERO_PIVOT;
+    Lap lap;
     level_sets(F->lvL, n, F->L.rowptr, F->L.col, kDepLower, st);
     level_sets(F->lvU, n, F->U.rowptr, F->U.col, kDepUpper, st);
     F->Udiag = dalloc<double>(n);
@@ -359,7 +403,9 @@ int make_factor(pmg_csr_s* A, double tau, double fillfactor, int ordering, pmg_f
     // wavefront kernels need the natural (unpermuted) order and grid-row segments
     if (F->perm || force_levelsched()) F->starts.clear();
     const bool natural = F->seg > 0 || !F->starts.empty();
+    lap("factor level sets", n);
     build_sells(natural);
+    lap("factor sells", n);
     // longest rows (reporting, layouts)
     std::vector<int32_t> lr(n + 1), ur(n + 1);
     PMG_CUDA(cudaMemcpyAsync(lr.data(), F->L.rowptr, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToHost, st));
@@ -424,8 +470,15 @@ int make_factor(pmg_csr_s* A, double tau, double fillfactor, int ordering, pmg_f
         F->seg = 0;
         if (natural) build_sells(false);
     }
+    lap("factor layouts + plans", n);
     *out = F.release();
     return PMG_OK;
+}
+
+int make_factor(pmg_csr_s* A, double tau, double fillfactor, int ordering, pmg_factor_s** out, int64_t* err_row,
+                cudaStream_t st) {
+    PendingFactor pf = factor_begin(A, tau, fillfactor, ordering, 0, st);
+    return factor_end(pf, out, err_row, st);
 }
 
 }  // namespace
@@ -1224,16 +1277,8 @@ int pmg_hier_create(const pmg_hier_desc* d, pmg_hier* out, int* err_level, int64
                 L.PT = make_csr(d->PT[l], s.s);
             }
         }
-        double ilut_s = 0;
         for (int l = 0; l + 1 < np; ++l) {
-            if (H->smoother == PMG_SMOOTHER_ILUT) {
-                int rc = make_factor(H->pl[l].A, d->tau, d->fillfactor, d->ordering, &H->pl[l].F, err_row, s.s);
-                if (rc) {
-                    if (err_level) *err_level = l;
-                    return rc;
-                }
-                ilut_s += H->pl[l].F->seconds;
-            } else {
+            if (H->smoother != PMG_SMOOTHER_ILUT) {
                 ensure_gs(H->pl[l].A, s.s);
                 if (H->pl[l].A->gs_zero_row >= 0) {
                     if (err_level) *err_level = l;
@@ -1257,19 +1302,80 @@ int pmg_hier_create(const pmg_hier_desc* d, pmg_hier* out, int* err_level, int64
                 check_view(&d->HPT[j]);
                 L.P = make_csr(d->HP[j], s.s);
                 L.PT = make_csr(d->HPT[j], s.s);
-                int rc = make_factor(L.A, d->tau, d->fillfactor, d->ordering, &L.F, err_row, s.s);
+            }
+        }
+        PMG_CUDA(cudaStreamSynchronize(s.s));
+        // ILUT of every level at once: each factorisation is a row-to-row chain that keeps only a
+        // few dozen CTAs busy, so the levels' chains run side by side on their own streams (the
+        // largest first; grids capped so that all of them are resident together)
+        struct Slot {
+            pmg_csr_s* A;
+            pmg_factor_s** F;
+            int level;
+            PendingFactor pf;
+            std::unique_ptr<Stream> st;
+        };
+        std::vector<Slot> slots;
+        if (H->smoother == PMG_SMOOTHER_ILUT)
+            for (int l = 0; l + 1 < np; ++l) slots.push_back({H->pl[l].A, &H->pl[l].F, l, {}, nullptr});
+        for (int j = 0; j + 1 < nh; ++j) slots.push_back({H->hl[j].A, &H->hl[j].F, np - 1 + j, {}, nullptr});
+        cudaEvent_t ref = nullptr;
+        PMG_CUDA(cudaEventCreate(&ref));
+        struct Cleanup {  // on an error path: wait for and drop the factorisations still in flight
+            std::vector<Slot>& sl;
+            cudaEvent_t ev;
+            ~Cleanup() {
+                for (auto& x : sl)
+                    if (x.pf.job) {
+                        DevCsr l, u;
+                        try {
+                            ilut_finish(x.pf.job, l, u, nullptr, nullptr, nullptr, nullptr);
+                        } catch (...) {
+                        }
+                        x.pf.job = nullptr;
+                        l.free();
+                        u.free();
+                        x.pf.owned.free();
+                    }
+                cudaEventDestroy(ev);
+            }
+        } cleanup{slots, ref};
+        static const bool serial = env_int("PMG_ILUT_SERIAL", 0) != 0;
+        const int nsm = sm_count();
+        double ilut_s = 0;
+        if (serial || slots.size() < 2) {
+            for (auto& x : slots) {
+                int rc = make_factor(x.A, d->tau, d->fillfactor, d->ordering, x.F, err_row, s.s);
                 if (rc) {
-                    if (err_level) *err_level = np - 1 + j;
+                    if (err_level) *err_level = x.level;
                     return rc;
                 }
-                ilut_s += L.F->seconds;
-            } else {
-                int k = dense_setup(H->coarse, L.A->A, s.s);
-                if (k >= 0) {
-                    if (err_level) *err_level = np - 1 + j;
-                    if (err_row) *err_row = k;
-                    return int(PMG_ZERO_PIVOT);
+                ilut_s += (*x.F)->seconds;
+            }
+        } else {
+            for (size_t q = 0; q < slots.size(); ++q) {
+                Slot& x = slots[q];
+                x.st = std::make_unique<Stream>();
+                if (q == 0) PMG_CUDA(cudaEventRecord(ref, x.st->s));
+                const bool heavy = x.A->A.nnz >= int64_t(32) * std::max(x.A->A.n, 1);
+                x.pf = factor_begin(x.A, d->tau, d->fillfactor, d->ordering, heavy ? nsm + nsm / 2 : 32, x.st->s);
+            }
+            for (auto& x : slots) {
+                double since = 0;
+                int rc = factor_end(x.pf, x.F, err_row, s.s, ref, &since);
+                if (rc) {
+                    if (err_level) *err_level = x.level;
+                    return rc;
                 }
+                ilut_s = std::max(ilut_s, since);
+            }
+        }
+        {
+            const int k = dense_setup(H->coarse, H->hl[nh - 1].A->A, s.s);
+            if (k >= 0) {
+                if (err_level) *err_level = np - 1 + nh - 1;
+                if (err_row) *err_row = k;
+                return int(PMG_ZERO_PIVOT);
             }
         }
         PMG_CUDA(cudaStreamSynchronize(s.s));

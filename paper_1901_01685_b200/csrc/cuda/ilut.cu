@@ -17,6 +17,12 @@
 // kept set under a strict total order is unique, so any exact selection matches).
 #include <cub/device/device_scan.cuh>
 
+#include <cstdio>
+#include <cstdlib>
+#include <memory>
+#include <mutex>
+#include <vector>
+
 #include "ilut.cuh"
 
 namespace pmg {
@@ -28,6 +34,9 @@ constexpr unsigned FULL = 0xffffffffu;
 // candidates of a selection are also kept in shared memory when they fit (the selection after the
 // last pivot is on the row-to-row critical path: no L2 round trips there)
 constexpr int kCandSh = 1024;
+// up to this many candidates the selection runs in warp 0 alone (no block barriers: the p = 1
+// factors); larger sets use the block-wide radix select
+constexpr int kCandWarp = 64;
 
 struct IlutDev {
     int32_t n, M, b, W, nwords;
@@ -48,7 +57,20 @@ struct IlutDev {
     int32_t* gcand_col;  // [slots * W]
     double* gcand_val;
     int smem_w;
+    unsigned long long* trace;  // PMG_ILUT_TRACE: 6 timestamps for kTraceRows rows from trace_row0 on
+    int32_t trace_row0;
 };
+constexpr int kTraceRows = 4096;
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define ILUT_STAMP(slot)                                                                   \
+    do {                                                                                   \
+        if (d.trace && threadIdx.x == 0 && i >= d.trace_row0 && i < d.trace_row0 + kTraceRows) \
+            d.trace[size_t(i - d.trace_row0) * 6 + (slot)] = gtime();                      \
+    } while (0)
 
 __device__ __forceinline__ uint64_t absbits(double x) {
     return (unsigned long long)__double_as_longlong(x) & 0x7FFFFFFFFFFFFFFFull;
@@ -62,63 +84,184 @@ __device__ __forceinline__ int block_scan_excl(int v, int* sh, int& total) {
         int y = __shfl_up_sync(FULL, x, o);
         if (lane >= o) x += y;
     }
-    __syncthreads();
     if (lane == 31) sh[wid] = x;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        int acc = 0;
-        for (int w = 0; w < kThreads / 32; ++w) {
-            int t = sh[w];
-            sh[w] = acc;
-            acc += t;
-        }
-        sh[kThreads / 32] = acc;
+    int base = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) {
+        const int c = sh[w];
+        if (w < wid) base += c;
+        tot += c;
     }
-    __syncthreads();
-    total = sh[kThreads / 32];
-    return sh[wid] + x - v;
+    __syncthreads();  // sh is reused by the next scan
+    total = tot;
+    return base + x - v;
 }
 
 // gather the band entries [lo, hi) that are present (and, if filter, |w| >= tau) into the
-// candidate arrays in ascending order; returns the count
-__device__ int gather(const double* w, const uint32_t* pres, int lo, int hi, bool filter, double tau, int col0,
-                      int32_t* ccol, double* cval, int32_t* scol, double* sval, int* sh) {
-    int base = 0;
+// candidate arrays in ascending order; returns the count.  Lane = entry of a 32-entry word:
+// the kept mask of every word by ballot (words interleaved over the warps), an exclusive scan of the
+// word counts, then every kept entry is written at its rank -- no per-thread serial bit loops.
+__device__ int gather(const double* w, const uint32_t* pres, uint32_t* kmask, int32_t* woff, int32_t* wlist, int lo, int hi,
+                      bool filter, double tau, int col0, int32_t* ccol, double* cval, int32_t* scol, double* sval, int* sh) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int w0 = lo >> 5, w1 = (hi + 31) >> 5;
+    auto word = [&](int wi) {
+        uint32_t bits = pres[wi];
+        if (wi == (lo >> 5)) bits &= FULL << (lo & 31);
+        if (wi == ((hi - 1) >> 5) && (hi & 31)) bits &= FULL >> (32 - (hi & 31));
+        return bits;
+    };
+    // the non-empty words, ascending (the band window is mostly empty)
+    int nlist = 0;
     for (int wb = w0; wb < w1; wb += kThreads) {
         const int wi = wb + threadIdx.x;
-        uint32_t bits = 0;
-        if (wi < w1) {
-            bits = pres[wi];
-            if (wi == (lo >> 5)) bits &= FULL << (lo & 31);
-            if (wi == ((hi - 1) >> 5) && (hi & 31)) bits &= FULL >> (32 - (hi & 31));
-            if (filter) {
-                uint32_t m = bits, keep = 0;
-                while (m) {
-                    int q = __ffs(m) - 1;
-                    m &= m - 1;
-                    if (!(fabs(w[wi * 32 + q]) < tau)) keep |= 1u << q;
-                }
-                bits = keep;
-            }
-        }
+        const bool nz = wi < w1 && word(wi) != 0u;
         int tot;
-        int o = block_scan_excl(__popc(bits), sh, tot) + base;
-        while (bits) {
-            int q = __ffs(bits) - 1;
-            bits &= bits - 1;
-            ccol[o] = col0 + wi * 32 + q;
-            cval[o] = w[wi * 32 + q];
-            if (o < kCandSh) {
-                scol[o] = col0 + wi * 32 + q;
-                sval[o] = w[wi * 32 + q];
-            }
-            ++o;
+        const int o = block_scan_excl(nz ? 1 : 0, sh, tot) + nlist;
+        if (nz) wlist[o] = wi;
+        nlist += tot;
+    }
+    __syncthreads();
+    for (int e = wid; e < nlist; e += kThreads / 32) {
+        const int wi = wlist[e];
+        uint32_t bits = word(wi);
+        if (filter) {
+            const bool keep = ((bits >> lane) & 1u) && !(fabs(w[wi * 32 + lane]) < tau);
+            bits = __ballot_sync(FULL, keep);
         }
+        if (lane == 0) kmask[e] = bits;
+    }
+    __syncthreads();
+    int base = 0;
+    for (int eb = 0; eb < nlist; eb += kThreads) {
+        const int e = eb + threadIdx.x;
+        int tot;
+        const int o = block_scan_excl(e < nlist ? __popc(kmask[e]) : 0, sh, tot) + base;
+        if (e < nlist) woff[e] = o;
         base += tot;
     }
     __syncthreads();
+    for (int e = wid; e < nlist; e += kThreads / 32) {
+        const uint32_t km = kmask[e];
+        if ((km >> lane) & 1u) {
+            const int wi = wlist[e];
+            const int o = woff[e] + __popc(km & ((1u << lane) - 1u));
+            const int32_t c = col0 + wi * 32 + lane;
+            const double v = w[wi * 32 + lane];
+            ccol[o] = c;
+            cval[o] = v;
+            if (o < kCandSh) {
+                scol[o] = c;
+                sval[o] = v;
+            }
+        }
+    }
+    __syncthreads();
     return base;
+}
+
+// rule 2 for candidates held in shared memory (C <= kCandSh), by warp 0 alone: the same MSD radix
+// select and ordered write as select_write below without a single block barrier inside.  The other
+// warps wait at the barrier at the end.  Returns the kept count.
+__device__ int select_write_warp(const int32_t* scol, const double* sval, int C, int M, int32_t* ocol, double* oval,
+                                 int* hist, int* s_n) {
+    if (C <= M) {
+        for (int t = threadIdx.x; t < C; t += kThreads) {
+            ocol[t] = scol[t];
+            oval[t] = sval[t];
+        }
+        __syncthreads();
+        return C;
+    }
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        const uint32_t lt = (1u << lane) - 1u;
+        uint64_t pre = 0, msk = 0, T = 0;
+        int need = M, bsz = 0;
+        bool unique = false;
+        for (int shift = 56; shift >= 0; shift -= 8) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) hist[lane * 8 + j] = 0;
+            __syncwarp();
+            for (int c0 = 0; c0 < C; c0 += 32) {
+                // lanes of one bin count themselves once (neighbouring magnitudes share their top
+                // bytes: un-aggregated, the 32 updates of one bin serialise)
+                const int t = c0 + lane;
+                const uint64_t k = t < C ? absbits(sval[t]) : 0;
+                const int bin = (t < C && (k & msk) == pre) ? int((k >> shift) & 255) : 256;
+                const uint32_t peers = __match_any_sync(FULL, bin);
+                if (bin < 256 && lane == __ffs(peers) - 1) hist[bin] += __popc(peers);
+                __syncwarp();
+            }
+            int loc[8], sum = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                loc[j] = hist[255 - 8 * lane - j];
+                sum += loc[j];
+            }
+            int incl = sum;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(FULL, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const int src = __ffs(__ballot_sync(FULL, incl >= need)) - 1;
+            int dsel = 0, cum = incl - sum, bs = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {  // the bin of this lane's eight where the count is reached
+                const bool hit = bs == 0 && cum + loc[j] >= need;
+                if (hit) {
+                    dsel = 255 - 8 * lane - j;
+                    bs = loc[j];
+                }
+                if (bs == 0) cum += loc[j];
+            }
+            dsel = __shfl_sync(FULL, dsel, src);
+            cum = __shfl_sync(FULL, cum, src);
+            bsz = __shfl_sync(FULL, bs, src);
+            pre |= uint64_t(dsel) << shift;
+            msk |= uint64_t(255) << shift;
+            need -= cum;
+            __syncwarp();
+            if (bsz == 1 && shift > 0) {  // one element left in the threshold bin: it is the threshold
+                uint64_t key = 0;
+                for (int t = lane; t < C; t += 32) {
+                    const uint64_t k = absbits(sval[t]);
+                    if ((k & msk) == pre) key = k;
+                }
+                const int who = __ffs(__ballot_sync(FULL, key != 0 || false)) - 1;
+                // the matching lane (a zero key cannot be the threshold of a non-empty tail: zeros
+                // sort last and are only reached when every candidate is kept, C <= M)
+                T = __shfl_sync(FULL, key, who < 0 ? 0 : who);
+                unique = true;
+                break;
+            }
+        }
+        if (!unique) T = pre;
+        const bool eq_all = unique || need == bsz;
+        int base = 0, eqbase = 0;
+        for (int c0 = 0; c0 < C; c0 += 32) {
+            const int t = c0 + lane;
+            const bool in = t < C;
+            const uint64_t k = in ? absbits(sval[t]) : 0;
+            const bool eq = in && k == T;
+            const uint32_t eb = __ballot_sync(FULL, eq);
+            const int eqr = eqbase + __popc(eb & lt);
+            const bool keep = in && (k > T || (eq && (eq_all || eqr < need)));
+            const uint32_t kb = __ballot_sync(FULL, keep);
+            if (keep) {
+                const int o = base + __popc(kb & lt);
+                ocol[o] = scol[t];
+                oval[o] = sval[t];
+            }
+            base += __popc(kb);
+            eqbase += __popc(eb);
+        }
+        if (lane == 0) *s_n = base;
+    }
+    __syncthreads();
+    return *s_n;
 }
 
 // rule 2: keep the M largest |v| (ties by ascending column = candidate order); write the
@@ -128,6 +271,7 @@ __device__ int select_write(const int32_t* ccol, const double* cval, int C, int 
     const bool keep_all = C <= M;
     uint64_t T = 0;
     int need = 0;
+    bool eq_all = true;
     if (!keep_all) {
         if (threadIdx.x == 0) {
             s64[0] = 0;  // prefix
@@ -135,7 +279,23 @@ __device__ int select_write(const int32_t* ccol, const double* cval, int C, int 
             s64[2] = uint64_t(M);
         }
         __syncthreads();
-        for (int shift = 56; shift >= 0; shift -= 8) {
+        // magnitudes of one row share the top byte of their keys nearly always: then that pass is
+        // a single vote
+        int shift0 = 56;
+        {
+            const uint64_t top = absbits(cval[0]) >> 56;
+            bool same = true;
+            for (int t = threadIdx.x; t < C; t += kThreads) same = same && (absbits(cval[t]) >> 56) == top;
+            if (__syncthreads_and(same)) {
+                if (threadIdx.x == 0) {
+                    s64[0] = top << 56;
+                    s64[1] = uint64_t(255) << 56;
+                }
+                shift0 = 48;
+                __syncthreads();
+            }
+        }
+        for (int shift = shift0; shift >= 0; shift -= 8) {
             hist[threadIdx.x] = 0;  // kThreads == 256 bins
             __syncthreads();
             const uint64_t pre = s64[0], msk = s64[1];
@@ -190,6 +350,8 @@ __device__ int select_write(const int32_t* ccol, const double* cval, int C, int 
         }
         T = s64[0];
         need = int(s64[2]);
+        // the threshold bin of the last pass holds exactly the elements equal to T
+        eq_all = uint64_t(need) == s64[3];
     }
     int base = 0, eqbase = 0;
     for (int c0 = 0; c0 < C; c0 += kThreads) {
@@ -197,9 +359,10 @@ __device__ int select_write(const int32_t* ccol, const double* cval, int C, int 
         const bool in = t < C;
         const uint64_t k = in ? absbits(cval[t]) : 0;
         const bool eq = in && !keep_all && k == T;
-        int eqtot, ktot;
-        const int eqr = block_scan_excl(eq ? 1 : 0, sh, eqtot) + eqbase;
-        const bool keep = in && (keep_all || k > T || (eq && eqr < need));
+        int eqtot = 0, ktot;
+        // rank among the elements equal to the threshold: only when some of them are dropped
+        const int eqr = eq_all ? 0 : block_scan_excl(eq ? 1 : 0, sh, eqtot) + eqbase;
+        const bool keep = in && (keep_all || k > T || (eq && (eq_all || eqr < need)));
         const int kr = block_scan_excl(keep ? 1 : 0, sh, ktot);
         if (keep) {
             ocol[base + kr] = ccol[t];
@@ -217,11 +380,14 @@ __global__ void __launch_bounds__(kThreads) k_ilut(IlutDev d) {
     __shared__ int sh[kThreads / 32 + 1];
     __shared__ int hist[256];
     __shared__ uint64_t s64[5];
-    __shared__ int s_row, s_k, s_go, s_ulen;
-    __shared__ double s_wk;
+    __shared__ int s_row, s_k;
     uint32_t* pres = reinterpret_cast<uint32_t*>(smem);
     uint32_t* piv = pres + d.nwords;
-    double* w = d.smem_w ? reinterpret_cast<double*>(smem + ((size_t(2 * d.nwords) * 4 + 15) & ~size_t(15)))
+    uint32_t* kmask = piv + d.nwords;                              // gather: kept mask per word
+    int32_t* woff = reinterpret_cast<int32_t*>(kmask + d.nwords);  // gather: output offset per word
+    int32_t* wlist = woff + d.nwords;                              // gather: the non-empty words
+    __shared__ int s_n;
+    double* w = d.smem_w ? reinterpret_cast<double*>(smem + ((size_t(5 * d.nwords) * 4 + 15) & ~size_t(15)))
                          : d.gw + size_t(blockIdx.x) * d.W;
     int32_t* ccol = d.gcand_col + size_t(blockIdx.x) * d.W;
     double* cval = d.gcand_val + size_t(blockIdx.x) * d.W;
@@ -247,6 +413,7 @@ __global__ void __launch_bounds__(kThreads) k_ilut(IlutDev d) {
         }
         const double tau_i = d.tau[i];
         __syncthreads();
+        ILUT_STAMP(0);
         int kb = 0;
         const int nwl = (b + 31) >> 5;
         for (;;) {
@@ -268,31 +435,34 @@ __global__ void __launch_bounds__(kThreads) k_ilut(IlutDev d) {
             __syncthreads();
             const int k = s_k;
             if (k < 0) break;
-            if (threadIdx.x == 0) {
-                piv[k >> 5] &= ~(1u << (k & 31));
-                const int jk = i - b + k;
-                while (ld_acquire(d.done + jk) == 0) __nanosleep(40);
-                const size_t ub = size_t(jk) * (M + 1);
-                const double wk = w[k] / __ldcg(d.Uval + ub);
-                if (fabs(wk) < tau_i) {
-                    w[k] = 0.0;
-                    pres[k >> 5] &= ~(1u << (k & 31));
-                    s_go = 0;
-                } else {
-                    w[k] = wk;
-                    s_wk = wk;
-                    s_go = 1;
-                    s_ulen = __ldcg(d.Ulen + jk);
-                }
+            // every thread waits for U row jk and loads its own entry together with the diagonal and
+            // the length: one L2 round trip per pivot.  All threads form the same multiplier.
+            const int jk = i - b + k;
+            if ((threadIdx.x & 31) == 0)  // one poller per warp; the warp's loads below follow it
+                while (ld_acquire(d.done + jk) == 0) __nanosleep(20);
+            __syncwarp();
+            ILUT_STAMP(1);
+            const size_t ub = size_t(jk) * (M + 1);
+            const double udiag = __ldcg(d.Uval + ub);
+            const int ulen = __ldcg(d.Ulen + jk);
+            int jb0 = 0;
+            double uv0 = 0.0;
+            if (threadIdx.x + 1 < ulen) {
+                jb0 = __ldcg(d.Ucol + ub + 1 + threadIdx.x) - i + b;
+                uv0 = __ldcg(d.Uval + ub + 1 + threadIdx.x);
             }
-            __syncthreads();
-            if (s_go) {
-                const int jk = i - b + k;
-                const size_t ub = size_t(jk) * (M + 1) + 1;
-                const double wk = s_wk;
-                for (int q = threadIdx.x; q < s_ulen - 1; q += kThreads) {
-                    const int jb = __ldcg(d.Ucol + ub + q) - i + b;
-                    const double uv = __ldcg(d.Uval + ub + q);
+            const double wk = w[k] / udiag;  // w[k] is not written before the barrier below
+            const bool go = !(fabs(wk) < tau_i);
+            if (go) {
+                if (threadIdx.x + 1 < ulen) {
+                    const uint32_t bit = 1u << (jb0 & 31);
+                    const uint32_t old = atomicOr(&pres[jb0 >> 5], bit);
+                    if (!(old & bit) && jb0 < b) atomicOr(&piv[jb0 >> 5], bit);
+                    w[jb0] = w[jb0] - wk * uv0;
+                }
+                for (int q = threadIdx.x + kThreads; q < ulen - 1; q += kThreads) {
+                    const int jb = __ldcg(d.Ucol + ub + 1 + q) - i + b;
+                    const double uv = __ldcg(d.Uval + ub + 1 + q);
                     const uint32_t bit = 1u << (jb & 31);
                     const uint32_t old = atomicOr(&pres[jb >> 5], bit);
                     if (!(old & bit) && jb < b) atomicOr(&piv[jb >> 5], bit);
@@ -300,33 +470,48 @@ __global__ void __launch_bounds__(kThreads) k_ilut(IlutDev d) {
                 }
             }
             __syncthreads();
+            if (threadIdx.x == 0) {  // U row jk has no column <= jk: nobody touched w[k] or its bits
+                piv[k >> 5] &= ~(1u << (k & 31));
+                if (go) {
+                    w[k] = wk;
+                } else {
+                    w[k] = 0.0;
+                    pres[k >> 5] &= ~(1u << (k & 31));
+                }
+            }
+            __syncwarp();  // warp 0 searches the pivot bitmap next
             kb = k + 1;
         }
         // ---- U part: diagonal + selected off-diagonals, published first
+        ILUT_STAMP(2);
         double diag = w[b];
         const bool has_diag = (pres[b >> 5] >> (b & 31)) & 1u;
         if (!has_diag || diag == 0.0) {
             if (threadIdx.x == 0) atomicMin(d.err_row, i);
             diag = 1.0;  // keep going so that no other CTA deadlocks; the host reports err_row
         }
-        int C = gather(w, pres, b + 1, d.W, true, tau_i, i - b, ccol, cval, scol, sval, sh);
+        int C = gather(w, pres, kmask, woff, wlist, b + 1, d.W, true, tau_i, i - b, ccol, cval, scol, sval, sh);
         const size_t ub = size_t(i) * (M + 1);
-        int nu = select_write(C <= kCandSh ? scol : ccol, C <= kCandSh ? sval : cval, C, M, d.Ucol + ub + 1,
-                              d.Uval + ub + 1, sh, hist, s64);
+        ILUT_STAMP(3);
+        int nu = C <= kCandWarp ? select_write_warp(scol, sval, C, M, d.Ucol + ub + 1, d.Uval + ub + 1, hist, &s_n)
+                                : select_write(C <= kCandSh ? scol : ccol, C <= kCandSh ? sval : cval, C, M,
+                                               d.Ucol + ub + 1, d.Uval + ub + 1, sh, hist, s64);
+        ILUT_STAMP(4);
         __threadfence();  // every writer orders its U entries before the release below
         __syncthreads();
         if (threadIdx.x == 0) {
             d.Ucol[ub] = i;
             d.Uval[ub] = diag;
             d.Ulen[i] = nu + 1;
-            __threadfence();
-            st_release(d.done + i, 1);
+            st_release(d.done + i, 1);  // orders this thread's three stores; the others fenced above
         }
+        ILUT_STAMP(5);
         // ---- L part: the kept multipliers
-        C = gather(w, pres, 0, b, false, 0.0, i - b, ccol, cval, scol, sval, sh);
+        C = gather(w, pres, kmask, woff, wlist, 0, b, false, 0.0, i - b, ccol, cval, scol, sval, sh);
         const size_t lb = size_t(i) * M;
-        int nl = select_write(C <= kCandSh ? scol : ccol, C <= kCandSh ? sval : cval, C, M, d.Lcol + lb, d.Lval + lb,
-                              sh, hist, s64);
+        int nl = C <= kCandWarp ? select_write_warp(scol, sval, C, M, d.Lcol + lb, d.Lval + lb, hist, &s_n)
+                                : select_write(C <= kCandSh ? scol : ccol, C <= kCandSh ? sval : cval, C, M, d.Lcol + lb,
+                                               d.Lval + lb, sh, hist, s64);
         if (threadIdx.x == 0) d.Llen[i] = nl;
         // ---- reset the window
         for (int wi = threadIdx.x; wi < d.nwords; wi += kThreads) {
@@ -393,24 +578,38 @@ void compact_rows(int32_t n, int stride, const int32_t* len, const int32_t* pcol
 
 }  // namespace
 
-int ilut_factorize_device(const DevCsr& A, int32_t band, double tau, double fillfactor, DevCsr& L, DevCsr& U,
-                          int64_t* err_row, double* seconds, cudaStream_t st) {
+struct IlutJob {
+    IlutDev d{};
+    int32_t n = 0, M = 0;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    cudaStream_t st = nullptr;
+    int* h_err = nullptr;  // pinned: first failing row
+};
+
+// Launch the factorisation of A on `st` and return without waiting: factorisations of independent
+// matrices (the levels of a hierarchy) run concurrently, each a row-to-row chain that needs only a
+// few dozen CTAs.  `max_ctas` caps the grid (0 = as many as fit).
+IlutJob* ilut_launch(const DevCsr& A, int32_t band, double tau, double fillfactor, int max_ctas, cudaStream_t st) {
+    auto* job = new IlutJob;
     const int32_t n = A.n;
     const int32_t M = int32_t(std::ceil(fillfactor * double(A.nnz) / double(n)));
     const int32_t b = std::max(band, 1);
     const int32_t W = 2 * b + 1;
     const int32_t nwords = (W + 31) / 32;
-    cudaEvent_t e0, e1;
-    PMG_CUDA(cudaEventCreate(&e0));
-    PMG_CUDA(cudaEventCreate(&e1));
-    PMG_CUDA(cudaEventRecord(e0, st));
+    job->n = n;
+    job->M = M;
+    job->st = st;
+    PMG_CUDA(cudaEventCreate(&job->e0));
+    PMG_CUDA(cudaEventCreate(&job->e1));
+    PMG_CUDA(cudaMallocHost(&job->h_err, sizeof(int)));
+    PMG_CUDA(cudaEventRecord(job->e0, st));
 
     int dev = 0, nsm = 0;
     PMG_CUDA(cudaGetDevice(&dev));
     PMG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     int max_smem = 0;
     PMG_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-    const size_t bits_bytes = (size_t(2 * nwords) * 4 + 15) & ~size_t(15);
+    const size_t bits_bytes = (size_t(5 * nwords) * 4 + 15) & ~size_t(15);
     const size_t static_bytes = 4096 + size_t(kCandSh) * 12;
     size_t dyn = bits_bytes + size_t(W) * 8;
     int smem_w = 1;
@@ -419,13 +618,23 @@ int ilut_factorize_device(const DevCsr& A, int32_t band, double tau, double fill
         dyn = bits_bytes;
     }
     if (dyn + static_bytes > size_t(max_smem)) throw CudaError("ilut: band too wide for the bitmaps", 6);
-    PMG_CUDA(cudaFuncSetAttribute(k_ilut, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dyn)));
+    {
+        // the attribute is per function, not per launch: only ever raise it (concurrent launches)
+        static std::mutex mu;
+        static size_t cur = 0;
+        std::lock_guard<std::mutex> lk(mu);
+        if (dyn > cur) {
+            PMG_CUDA(cudaFuncSetAttribute(k_ilut, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dyn)));
+            cur = dyn;
+        }
+    }
     int occ = 0;
     PMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_ilut, kThreads, dyn));
-    occ = std::max(1, std::min(occ, 4));
-    const int grid = std::min<int64_t>(int64_t(nsm) * occ, std::max<int32_t>(n, 1));
+    occ = std::max(1, std::min(occ, 2));  // waiting CTAs only poll: two per SM keep the chain fed
+    int grid = int(std::min<int64_t>(int64_t(nsm) * occ, std::max<int32_t>(n, 1)));
+    if (max_ctas > 0) grid = std::min(grid, max_ctas);
 
-    IlutDev d{};
+    IlutDev& d = job->d;
     d.n = n; d.M = M; d.b = b; d.W = W; d.nwords = nwords;
     d.rp = A.rowptr; d.ci = A.col; d.v = A.val;
     d.smem_w = smem_w;
@@ -443,36 +652,84 @@ int ilut_factorize_device(const DevCsr& A, int32_t band, double tau, double fill
     d.err_row = d.ticket + 1;
     PMG_CUDA(cudaMallocAsync(&d.gcand_col, sizeof(int32_t) * size_t(grid) * W, st));
     PMG_CUDA(cudaMallocAsync(&d.gcand_val, sizeof(double) * size_t(grid) * W, st));
+    d.trace = nullptr;
+    if (getenv("PMG_ILUT_TRACE") && n > 4 * kTraceRows) {
+        PMG_CUDA(cudaMallocAsync(&d.trace, sizeof(unsigned long long) * kTraceRows * 6, st));
+        PMG_CUDA(cudaMemsetAsync(d.trace, 0, sizeof(unsigned long long) * kTraceRows * 6, st));
+        d.trace_row0 = n / 2;
+    }
     d.gw = nullptr;
     if (!smem_w) PMG_CUDA(cudaMallocAsync(&d.gw, sizeof(double) * size_t(grid) * W, st));
     PMG_CUDA(cudaMemsetAsync(d.done, 0, sizeof(int) * n, st));
-    int init[2] = {0, 0x7fffffff};
-    PMG_CUDA(cudaMemcpyAsync(d.ticket, init, sizeof(init), cudaMemcpyHostToDevice, st));
+    PMG_CUDA(cudaMemsetAsync(d.ticket, 0, sizeof(int), st));
+    PMG_CUDA(cudaMemsetAsync(d.err_row, 0x7f, sizeof(int), st));  // 0x7f7f7f7f: no failing row yet
     k_ilut<<<grid, kThreads, dyn, st>>>(d);
     PMG_LAUNCH_CHECK();
-    int er = 0;
-    PMG_CUDA(cudaMemcpyAsync(&er, d.err_row, sizeof(int), cudaMemcpyDeviceToHost, st));
+    PMG_CUDA(cudaEventRecord(job->e1, st));
+    PMG_CUDA(cudaMemcpyAsync(job->h_err, d.err_row, sizeof(int), cudaMemcpyDeviceToHost, st));
+    return job;
+}
+
+// Wait for a launched factorisation, compact its rows into L and U and release the job.
+int ilut_finish(IlutJob* job, DevCsr& L, DevCsr& U, int64_t* err_row, double* seconds, cudaEvent_t ref,
+                double* seconds_since_ref) {
+    std::unique_ptr<IlutJob> own(job);
+    IlutDev& d = job->d;
+    cudaStream_t st = job->st;
+    const int32_t n = job->n, M = job->M;
     PMG_CUDA(cudaStreamSynchronize(st));
+    if (d.trace) {  // diagnostics: where the row-to-row chain spends its time (ns, means over the window)
+        std::vector<unsigned long long> t(size_t(kTraceRows) * 6);
+        PMG_CUDA(cudaMemcpy(t.data(), d.trace, t.size() * 8, cudaMemcpyDeviceToHost));
+        double s[6] = {0, 0, 0, 0, 0, 0};
+        int cnt = 0;
+        for (int r = 1; r < kTraceRows; ++r) {
+            const unsigned long long *a = &t[size_t(r) * 6], *p = &t[size_t(r - 1) * 6];
+            if (!a[5] || !p[5] || !a[1]) continue;
+            s[0] += double(a[5]) - double(p[5]);                         // chain period
+            s[1] += double(a[1]) - double(p[5]);                         // release -> observed by the next row
+            s[2] += double(a[2]) - double(a[1]);                         // last pivot
+            s[3] += double(a[3]) - double(a[2]);                         // gather U
+            s[4] += double(a[4]) - double(a[3]);                         // select + write
+            s[5] += double(a[5]) - double(a[4]);                         // fence + release
+            ++cnt;
+        }
+        if (cnt)
+            fprintf(stderr, "[pmg] ilut trace n=%d M=%d (%d rows): period %.0f ns = hand-over %.0f + last pivot %.0f + gather %.0f + "
+                    "select %.0f + publish %.0f\n", job->n, job->M, cnt, s[0] / cnt, s[1] / cnt, s[2] / cnt, s[3] / cnt, s[4] / cnt,
+                    s[5] / cnt);
+        PMG_CUDA(cudaFreeAsync(d.trace, st));
+        d.trace = nullptr;
+    }
+    const int er = *job->h_err;
     int status = 0;
-    if (er != 0x7fffffff) {
+    if (er != 0x7f7f7f7f) {
         if (err_row) *err_row = er;
         status = 1;  // PMG_ZERO_PIVOT
     } else {
         compact_rows(n, M, d.Llen, d.Lcol, d.Lval, L, st);
         compact_rows(n, M + 1, d.Ulen, d.Ucol, d.Uval, U, st);
     }
-    PMG_CUDA(cudaEventRecord(e1, st));
-    PMG_CUDA(cudaEventSynchronize(e1));
     float ms = 0;
-    PMG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    PMG_CUDA(cudaEventElapsedTime(&ms, job->e0, job->e1));  // the factorisation kernel (compaction excluded)
     if (seconds) *seconds = ms * 1e-3;
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
+    if (ref && seconds_since_ref) {
+        PMG_CUDA(cudaEventElapsedTime(&ms, ref, job->e1));
+        *seconds_since_ref = ms * 1e-3;
+    }
+    cudaEventDestroy(job->e0);
+    cudaEventDestroy(job->e1);
+    cudaFreeHost(job->h_err);
     for (void* p : {(void*)d.tau, (void*)d.Ucol, (void*)d.Uval, (void*)d.Ulen, (void*)d.Lcol, (void*)d.Lval,
                     (void*)d.Llen, (void*)d.done, (void*)d.ticket, (void*)d.gcand_col, (void*)d.gcand_val, (void*)d.gw})
         if (p) PMG_CUDA(cudaFreeAsync(p, st));
     PMG_CUDA(cudaStreamSynchronize(st));
     return status;
+}
+
+int ilut_factorize_device(const DevCsr& A, int32_t band, double tau, double fillfactor, DevCsr& L, DevCsr& U,
+                          int64_t* err_row, double* seconds, cudaStream_t st) {
+    return ilut_finish(ilut_launch(A, band, tau, fillfactor, 0, st), L, U, err_row, seconds, nullptr, nullptr);
 }
 
 }  // namespace pmg

@@ -29,4 +29,14 @@ struct DevCsr {
 int ilut_factorize_device(const DevCsr& A, int32_t band, double tau, double fillfactor, DevCsr& L, DevCsr& U,
                           int64_t* err_row, double* seconds, cudaStream_t st);
 
+// The same in two steps, so that independent factorisations overlap: ilut_launch enqueues the
+// work on `st` (grid capped at max_ctas, 0 = no cap) and returns; ilut_finish waits, compacts the
+// rows into L and U and frees the job.
+struct IlutJob;
+IlutJob* ilut_launch(const DevCsr& A, int32_t band, double tau, double fillfactor, int max_ctas, cudaStream_t st);
+// `seconds`: the factorisation kernel; `seconds_since_ref`: from the event `ref` (recorded by the
+// caller before the first of several concurrent launches) to the end of this kernel
+int ilut_finish(IlutJob* job, DevCsr& L, DevCsr& U, int64_t* err_row, double* seconds, cudaEvent_t ref,
+                double* seconds_since_ref);
+
 }  // namespace pmg
