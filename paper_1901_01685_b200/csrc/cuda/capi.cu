@@ -3,6 +3,7 @@
 // solve runs in the kernels of sell.cu / trsv.cu / dense.cu; the host only sequences
 // launches on the work stream.
 #include <chrono>
+#include <mutex>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -126,7 +127,18 @@ struct pmg_csr_s {
     DevCsr A;
     Sell S;                       // identity-order sliced layout (SpMV family)
     std::vector<int32_t> h_rowptr, h_col;
-    std::vector<double> h_val;    // host copy (setup: RCM / permutation)
+    std::vector<double> h_val;    // host copy, fetched from the device when RCM needs it
+    std::once_flag h_once;
+    void ensure_host() {
+        std::call_once(h_once, [&] {
+            h_rowptr.resize(size_t(A.n) + 1);
+            h_col.resize(size_t(A.nnz));
+            h_val.resize(size_t(A.nnz));
+            PMG_CUDA(cudaMemcpy(h_rowptr.data(), A.rowptr, sizeof(int32_t) * h_rowptr.size(), cudaMemcpyDeviceToHost));
+            PMG_CUDA(cudaMemcpy(h_col.data(), A.col, sizeof(int32_t) * h_col.size(), cudaMemcpyDeviceToHost));
+            PMG_CUDA(cudaMemcpy(h_val.data(), A.val, sizeof(double) * h_val.size(), cudaMemcpyDeviceToHost));
+        });
+    }
     int32_t band = 0;
     // Gauss-Seidel structures (built on first use)
     bool gs_ready = false;
@@ -164,7 +176,15 @@ struct pmg_factor_s {
     DevCsr L, U;
     int32_t* perm = nullptr;          // device, null for the identity ordering
     std::vector<int32_t> h_perm;
-    LevelSets lvL, lvU;
+    LevelSets lvL, lvU;               // built on first use: reporting, level-scheduled fallback
+    std::once_flag lv_once;
+    void ensure_levels(cudaStream_t st) {
+        std::call_once(lv_once, [&] {
+            level_sets(lvL, n, L.rowptr, L.col, kDepLower, st);
+            level_sets(lvU, n, U.rowptr, U.col, kDepUpper, st);
+            PMG_CUDA(cudaStreamSynchronize(st));
+        });
+    }
     Sell Ls, Us;
     double* Udiag = nullptr;          // 1.0 / diagonal of U per sweep position
     int32_t max_row_L = 0, max_row_U = 0;
@@ -245,10 +265,6 @@ pmg_csr_s* make_csr(const pmg_csr_view& v, cudaStream_t st) {
     Lap lap;
     h->A = upload(v, st);
     lap("csr upload", v.nrows);
-    h->h_rowptr.assign(v.rowptr, v.rowptr + v.nrows + 1);
-    h->h_col.assign(v.col, v.col + h->A.nnz);
-    h->h_val.assign(v.val, v.val + h->A.nnz);
-    lap("csr host copy", v.nrows);
     h->band = pmg_host::bandwidth(v.nrows, v.rowptr, v.col);
     h->seg = force_levelsched() ? 0 : detect_segment(v.nrows, v.rowptr, v.col);
     if (!force_levelsched() && v.nrows == v.ncols) h->starts = detect_segment_starts(v.nrows, v.rowptr, v.col);
@@ -347,6 +363,7 @@ PendingFactor factor_begin(pmg_csr_s* A, double tau, double fillfactor, int orde
     F->seg = A->seg;
     F->starts = A->starts;
     if (ordering == PMG_ORDER_RCM) {
+        A->ensure_host();
         F->h_perm = pmg_host::rcm_ordering(n, A->h_rowptr.data(), A->h_col.data());
         std::vector<int32_t> brp, bci;
         std::vector<double> bv;
@@ -380,12 +397,11 @@ int factor_end(PendingFactor& pf, pmg_factor_s** out, int64_t* err_row, cudaStre
                 F->seconds, 1e6 * F->seconds / std::max(n, 1));
     if (rc != 0) return PMG_ZERO_PIVOT;
     Lap lap;
-    level_sets(F->lvL, n, F->L.rowptr, F->L.col, kDepLower, st);
-    level_sets(F->lvU, n, F->U.rowptr, F->U.col, kDepUpper, st);
     F->Udiag = dalloc<double>(n);
     // sliced layouts: natural order (L ascending, U descending rows) for the wavefront kernels,
     // level order for the level-scheduled fallback
     auto build_sells = [&](bool natural) {
+        if (!natural) F->ensure_levels(st);
         sell_free(F->Ls);
         sell_free(F->Us);
         if (natural && !F->rev) {
@@ -403,7 +419,6 @@ int factor_end(PendingFactor& pf, pmg_factor_s** out, int64_t* err_row, cudaStre
     // wavefront kernels need the natural (unpermuted) order and grid-row segments
     if (F->perm || force_levelsched()) F->starts.clear();
     const bool natural = F->seg > 0 || !F->starts.empty();
-    lap("factor level sets", n);
     build_sells(natural);
     lap("factor sells", n);
     // longest rows (reporting, layouts)
@@ -1209,6 +1224,14 @@ int pmg_factor_stats(pmg_factor F, int64_t* nnz_L, int64_t* nnz_U, int32_t* leve
                      int32_t* max_row_L, int32_t* max_row_U) {
     if (nnz_L) *nnz_L = F->L.nnz;
     if (nnz_U) *nnz_U = F->U.nnz;
+    if (levels_L || levels_U) {
+        const int rc = guarded([&] {
+            Stream s;
+            F->ensure_levels(s.s);
+            return int(PMG_OK);
+        });
+        if (rc != PMG_OK) return rc;
+    }
     if (levels_L) *levels_L = F->lvL.nlevels;
     if (levels_U) *levels_U = F->lvU.nlevels;
     if (max_row_L) *max_row_L = F->max_row_L;

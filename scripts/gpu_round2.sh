@@ -4,7 +4,7 @@ cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out/r2
 timeout 1800 python -m pytest tests -m gpu -q 2>&1 | tail -8 > gpurun_out/r2/gpu_tests.txt
 cat gpurun_out/r2/gpu_tests.txt
-timeout 900 python bench.py --steps 5 --warmup 3 --cpu-single-thread > gpurun_out/r2/bench_default.json 2> gpurun_out/r2/bench_default.err; echo "default rc=$?"
+timeout 1200 python bench.py --steps 5 --warmup 3 --cpu-single-thread --time-host-assembly > gpurun_out/r2/bench_default.json 2> gpurun_out/r2/bench_default.err; echo "default rc=$?"
 run() {
   name=$1; shift
   timeout 900 python bench.py "$@" --steps 3 --warmup 3 --no-bicgstab > gpurun_out/r2/cfg_$name.json 2> gpurun_out/r2/cfg_$name.err; echo "$name rc=$?"

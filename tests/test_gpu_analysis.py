@@ -62,7 +62,7 @@ def test_smooth_and_coarse_correction_equal_oracle(smoother, degrees):
         if level + 1 < len(pb.plevels):
             np.testing.assert_array_equal(_bits(pmg.coarse_correction(H, level, u, f)),
                                           _bits(Ho.coarse_correction(u, f, level)))
-    with pytest.raises(pmg.PmgError):
+    with pytest.raises(ValueError):  # PMG_ERR_ARG: the last p-level has no coarser level
         pmg.coarse_correction(H, len(pb.plevels) - 1, np.zeros(pb.plevels[-1].A.nrows), np.zeros(pb.plevels[-1].A.nrows))
 
 
