@@ -39,14 +39,20 @@ namespace pmg {
 
 namespace {
 
-constexpr int G = 32;           // steps per bulk copy = unroll of the step loop
+#ifndef PMG_WAVE_G
+#define PMG_WAVE_G 32
+#endif
+#ifndef PMG_WAVE_WMAX
+#define PMG_WAVE_WMAX 2
+#endif
+constexpr int G = PMG_WAVE_G;   // steps per bulk copy = unroll of the step loop
 constexpr int NG = 2;           // item groups in flight
 constexpr int PF = G * NG;      // item ring steps
 constexpr int NRH = 4;          // right-hand-side ring groups
 constexpr int STEP_BYTES = 3 * 32 * 16;
 constexpr int MAXD = 8;         // segments back a term may reach
 constexpr int EMAX = 8;         // blocks back a term may reach
-constexpr int WMAX = 2;         // sweep warps per CTA
+constexpr int WMAX = PMG_WAVE_WMAX;  // sweep warps per CTA
 #ifndef PMG_WAVE_CHK
 #define PMG_WAVE_CHK 2
 #endif

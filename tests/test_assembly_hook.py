@@ -71,3 +71,24 @@ def test_geometry_error_is_reported(emu):
     fail = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p)(lambda rq: 3)
     with pytest.raises(RuntimeError, match="external assembler"):
         P.matrix("A", "square", 2, 2, assembly=fail)
+
+
+def test_structure_is_independent_of_the_thread_count(emu):
+    """patterns, transposes, load vector and values are bit-reproducible for any
+    number of host workers -- host loop and external producer alike."""
+    spec = P.make_spec("annulus", "annulus", (3, 2, 1), 4)
+    ref = None
+    try:
+        for nt in (1, 3, 8):
+            P.set_threads(nt)
+            for asm in (None, emu):
+                pb = P.build(spec, assembly=asm)
+                if ref is None:
+                    ref = pb
+                else:
+                    same_problem(ref, pb)
+                    for la, lb in zip(ref.plevels, pb.plevels):
+                        if la.PT is not None:
+                            assert (la.PT.col == lb.PT.col).all() and (la.PT.rowptr == lb.PT.rowptr).all()
+    finally:
+        P.set_threads(0)
