@@ -34,9 +34,10 @@ constexpr unsigned FULL = 0xffffffffu;
 // candidates of a selection are also kept in shared memory when they fit (the selection after the
 // last pivot is on the row-to-row critical path: no L2 round trips there)
 constexpr int kCandSh = 1024;
-// up to this many candidates the selection runs in warp 0 alone (no block barriers: the p = 1
-// factors); larger sets use the block-wide radix select
-constexpr int kCandWarp = 64;
+// up to this many candidates the selection is by ranks (one barrier round: the p = 1 factors);
+// larger sets use the block-wide radix select (ranks cost C^2 comparisons: ~1000 candidates per row
+// of the p = 5 factor took 58 us against 4.7 us)
+constexpr int kCandRank = 128;
 
 struct IlutDev {
     int32_t n, M, b, W, nwords;
@@ -161,11 +162,13 @@ __device__ int gather(const double* w, const uint32_t* pres, uint32_t* kmask, in
     return base;
 }
 
-// rule 2 for candidates held in shared memory (C <= kCandSh), by warp 0 alone: the same MSD radix
-// select and ordered write as select_write below without a single block barrier inside.  The other
-// warps wait at the barrier at the end.  Returns the kept count.
-__device__ int select_write_warp(const int32_t* scol, const double* sval, int C, int M, int32_t* ocol, double* oval,
-                                 int* hist, int* s_n) {
+// rule 2 by ranks, for candidates held in shared memory: every thread counts, for each of its
+// candidates, the candidates that precede it in the selection order (|v| descending, column
+// ascending) -- broadcast reads, no barrier, no histogram -- and keeps it iff fewer than M do; the
+// kept entries are written in column order through one scan per 256 candidates.  Exact: the order
+// is total, so the kept set is the one any exact selection finds.
+__device__ int select_write_rank(const int32_t* scol, const double* sval, int C, int M, int32_t* ocol, double* oval,
+                                 int* sh) {
     if (C <= M) {
         for (int t = threadIdx.x; t < C; t += kThreads) {
             ocol[t] = scol[t];
@@ -174,94 +177,29 @@ __device__ int select_write_warp(const int32_t* scol, const double* sval, int C,
         __syncthreads();
         return C;
     }
-    if (threadIdx.x < 32) {
-        const int lane = threadIdx.x;
-        const uint32_t lt = (1u << lane) - 1u;
-        uint64_t pre = 0, msk = 0, T = 0;
-        int need = M, bsz = 0;
-        bool unique = false;
-        for (int shift = 56; shift >= 0; shift -= 8) {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) hist[lane * 8 + j] = 0;
-            __syncwarp();
-            for (int c0 = 0; c0 < C; c0 += 32) {
-                // lanes of one bin count themselves once (neighbouring magnitudes share their top
-                // bytes: un-aggregated, the 32 updates of one bin serialise)
-                const int t = c0 + lane;
-                const uint64_t k = t < C ? absbits(sval[t]) : 0;
-                const int bin = (t < C && (k & msk) == pre) ? int((k >> shift) & 255) : 256;
-                const uint32_t peers = __match_any_sync(FULL, bin);
-                if (bin < 256 && lane == __ffs(peers) - 1) hist[bin] += __popc(peers);
-                __syncwarp();
+    int base = 0;
+    for (int c0 = 0; c0 < C; c0 += kThreads) {
+        const int t = c0 + threadIdx.x;
+        bool keep = false;
+        if (t < C) {
+            const uint64_t kt = absbits(sval[t]);
+            int rank = 0;
+            for (int j = 0; j < C; ++j) {
+                const uint64_t kj = absbits(sval[j]);
+                rank += (kj > kt || (kj == kt && j < t)) ? 1 : 0;
             }
-            int loc[8], sum = 0;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                loc[j] = hist[255 - 8 * lane - j];
-                sum += loc[j];
-            }
-            int incl = sum;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(FULL, incl, o);
-                if (lane >= o) incl += y;
-            }
-            const int src = __ffs(__ballot_sync(FULL, incl >= need)) - 1;
-            int dsel = 0, cum = incl - sum, bs = 0;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {  // the bin of this lane's eight where the count is reached
-                const bool hit = bs == 0 && cum + loc[j] >= need;
-                if (hit) {
-                    dsel = 255 - 8 * lane - j;
-                    bs = loc[j];
-                }
-                if (bs == 0) cum += loc[j];
-            }
-            dsel = __shfl_sync(FULL, dsel, src);
-            cum = __shfl_sync(FULL, cum, src);
-            bsz = __shfl_sync(FULL, bs, src);
-            pre |= uint64_t(dsel) << shift;
-            msk |= uint64_t(255) << shift;
-            need -= cum;
-            __syncwarp();
-            if (bsz == 1 && shift > 0) {  // one element left in the threshold bin: it is the threshold
-                uint64_t key = 0;
-                for (int t = lane; t < C; t += 32) {
-                    const uint64_t k = absbits(sval[t]);
-                    if ((k & msk) == pre) key = k;
-                }
-                const int who = __ffs(__ballot_sync(FULL, key != 0 || false)) - 1;
-                // the matching lane (a zero key cannot be the threshold of a non-empty tail: zeros
-                // sort last and are only reached when every candidate is kept, C <= M)
-                T = __shfl_sync(FULL, key, who < 0 ? 0 : who);
-                unique = true;
-                break;
-            }
+            keep = rank < M;
         }
-        if (!unique) T = pre;
-        const bool eq_all = unique || need == bsz;
-        int base = 0, eqbase = 0;
-        for (int c0 = 0; c0 < C; c0 += 32) {
-            const int t = c0 + lane;
-            const bool in = t < C;
-            const uint64_t k = in ? absbits(sval[t]) : 0;
-            const bool eq = in && k == T;
-            const uint32_t eb = __ballot_sync(FULL, eq);
-            const int eqr = eqbase + __popc(eb & lt);
-            const bool keep = in && (k > T || (eq && (eq_all || eqr < need)));
-            const uint32_t kb = __ballot_sync(FULL, keep);
-            if (keep) {
-                const int o = base + __popc(kb & lt);
-                ocol[o] = scol[t];
-                oval[o] = sval[t];
-            }
-            base += __popc(kb);
-            eqbase += __popc(eb);
+        int tot;
+        const int o = block_scan_excl(keep ? 1 : 0, sh, tot) + base;
+        if (keep) {
+            ocol[o] = scol[t];
+            oval[o] = sval[t];
         }
-        if (lane == 0) *s_n = base;
+        base += tot;
     }
     __syncthreads();
-    return *s_n;
+    return base;
 }
 
 // rule 2: keep the M largest |v| (ties by ascending column = candidate order); write the
@@ -386,7 +324,6 @@ __global__ void __launch_bounds__(kThreads) k_ilut(IlutDev d) {
     uint32_t* kmask = piv + d.nwords;                              // gather: kept mask per word
     int32_t* woff = reinterpret_cast<int32_t*>(kmask + d.nwords);  // gather: output offset per word
     int32_t* wlist = woff + d.nwords;                              // gather: the non-empty words
-    __shared__ int s_n;
     double* w = d.smem_w ? reinterpret_cast<double*>(smem + ((size_t(5 * d.nwords) * 4 + 15) & ~size_t(15)))
                          : d.gw + size_t(blockIdx.x) * d.W;
     int32_t* ccol = d.gcand_col + size_t(blockIdx.x) * d.W;
@@ -493,7 +430,7 @@ __global__ void __launch_bounds__(kThreads) k_ilut(IlutDev d) {
         int C = gather(w, pres, kmask, woff, wlist, b + 1, d.W, true, tau_i, i - b, ccol, cval, scol, sval, sh);
         const size_t ub = size_t(i) * (M + 1);
         ILUT_STAMP(3);
-        int nu = C <= kCandWarp ? select_write_warp(scol, sval, C, M, d.Ucol + ub + 1, d.Uval + ub + 1, hist, &s_n)
+        int nu = C <= kCandRank ? select_write_rank(scol, sval, C, M, d.Ucol + ub + 1, d.Uval + ub + 1, sh)
                                 : select_write(C <= kCandSh ? scol : ccol, C <= kCandSh ? sval : cval, C, M,
                                                d.Ucol + ub + 1, d.Uval + ub + 1, sh, hist, s64);
         ILUT_STAMP(4);
@@ -509,7 +446,7 @@ __global__ void __launch_bounds__(kThreads) k_ilut(IlutDev d) {
         // ---- L part: the kept multipliers
         C = gather(w, pres, kmask, woff, wlist, 0, b, false, 0.0, i - b, ccol, cval, scol, sval, sh);
         const size_t lb = size_t(i) * M;
-        int nl = C <= kCandWarp ? select_write_warp(scol, sval, C, M, d.Lcol + lb, d.Lval + lb, hist, &s_n)
+        int nl = C <= kCandRank ? select_write_rank(scol, sval, C, M, d.Lcol + lb, d.Lval + lb, sh)
                                 : select_write(C <= kCandSh ? scol : ccol, C <= kCandSh ? sval : cval, C, M, d.Lcol + lb,
                                                d.Lval + lb, sh, hist, s64);
         if (threadIdx.x == 0) d.Llen[i] = nl;

@@ -4,8 +4,8 @@ cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out/ab
 for lib in "$@"; do
   echo "== $lib"
-  PMG_CUDA_LIB=$lib timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -m "gpu and not slow" 2>&1 | tail -2
-  PMG_CUDA_LIB=$lib PMG_VERBOSE=1 timeout 900 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-bicgstab > gpurun_out/ab/$lib.json 2> gpurun_out/ab/$lib.err; echo "rc=$?"
+  PMG_CUDA_LIB=$lib timeout 240 python -m pytest tests/test_gpu_parity.py -x -q -m "gpu and not slow" 2>&1 | tail -2
+  PMG_CUDA_LIB=$lib PMG_VERBOSE=1 timeout 400 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-bicgstab > gpurun_out/ab/$lib.json 2> gpurun_out/ab/$lib.err; echo "rc=$?"
   grep "wave plan n=10" gpurun_out/ab/$lib.err | head -4
   python - <<PY
 import json
