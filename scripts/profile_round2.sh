@@ -25,7 +25,7 @@ PMG_PROFILE_REGION=1 timeout 1500 ncu --profile-from-start off --set full --cloc
     --kernel-name-base function -k regex:"^k_wave$|^k_wave_gs_su$" -c 3 -o $O/gs_full \
     python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-bicgstab --smoother gs > $O/ncu_gs.log 2>&1; echo "gs rc=$?"
 export_csv $O/gs_full
-timeout 1500 ncu --set full --clock-control none --kernel-name-base function -k regex:"^k_ilut$|^k_asm_" -c 12 \
+timeout 1500 ncu --set full --clock-control none --kernel-name-base function -k regex:"^k_ilut$|^k_asm_elements$|^k_asm_gather$|^k_asm_rowsum$" -c 40 \
     -o $O/setup_full python -c "
 import sys; sys.path.insert(0, '.')
 from paper_1901_01685_b200 import pmg, problems as P
