@@ -331,6 +331,7 @@ __global__ void __launch_bounds__(kThreads) k_ilut(IlutDev d) {
     __shared__ int32_t scol[kCandSh];
     __shared__ double sval[kCandSh];
     const int b = d.b, M = d.M;
+    double t_pre = 0.0;  // pre-threshold of the U-part selection (see below)
 
     for (int q = threadIdx.x; q < d.W; q += kThreads) w[q] = 0.0;
     for (int q = threadIdx.x; q < 2 * d.nwords; q += kThreads) pres[q] = 0;
@@ -427,12 +428,25 @@ __global__ void __launch_bounds__(kThreads) k_ilut(IlutDev d) {
             if (threadIdx.x == 0) atomicMin(d.err_row, i);
             diag = 1.0;  // keep going so that no other CTA deadlocks; the host reports err_row
         }
-        int C = gather(w, pres, kmask, woff, wlist, b + 1, d.W, true, tau_i, i - b, ccol, cval, scol, sval, sh);
+        // Rule 2 keeps the M largest of the entries >= tau_i.  A row of the p = 5 factor has ~1,000
+        // of them and keeps 121; a lower bound of the kept magnitudes, guessed from the last row
+        // this CTA selected (t_pre = half its M-th largest), drops most of the rest in the gather.
+        // Exact: if at least M entries pass the bound, the M largest pass it; otherwise gather again.
+        int C = gather(w, pres, kmask, woff, wlist, b + 1, d.W, true, fmax(tau_i, t_pre), i - b, ccol, cval, scol, sval, sh);
+        if (t_pre > tau_i && C < M)
+            C = gather(w, pres, kmask, woff, wlist, b + 1, d.W, true, tau_i, i - b, ccol, cval, scol, sval, sh);
         const size_t ub = size_t(i) * (M + 1);
         ILUT_STAMP(3);
-        int nu = C <= kCandRank ? select_write_rank(scol, sval, C, M, d.Ucol + ub + 1, d.Uval + ub + 1, sh)
-                                : select_write(C <= kCandSh ? scol : ccol, C <= kCandSh ? sval : cval, C, M,
-                                               d.Ucol + ub + 1, d.Uval + ub + 1, sh, hist, s64);
+        int nu;
+        if (C <= kCandRank) {
+            nu = select_write_rank(scol, sval, C, M, d.Ucol + ub + 1, d.Uval + ub + 1, sh);
+        } else {
+            nu = select_write(C <= kCandSh ? scol : ccol, C <= kCandSh ? sval : cval, C, M, d.Ucol + ub + 1,
+                              d.Uval + ub + 1, sh, hist, s64);
+            // s64[0] holds the bits of the M-th largest magnitude (C > M here); all threads read it
+            // before the next selection's first barrier-separated write
+            if (C > M) t_pre = __longlong_as_double((long long)s64[0]) * 0.5;
+        }
         ILUT_STAMP(4);
         __threadfence();  // every writer orders its U entries before the release below
         __syncthreads();
