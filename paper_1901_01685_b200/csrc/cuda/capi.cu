@@ -223,10 +223,13 @@ namespace {
 // e = U^{-1} L^{-1} r[perm] added into u[perm]  (y, x: scratch)
 void apply_factor(pmg_factor_s* F, const double* r, double* y, double* x, double* u, int* ticket, cudaStream_t st) {
     if (F->wave) {
+        wave_prepare2(y, x, F->n, ticket, st);  // sentinels in both outputs, both claim counters
         WaveOp l{kSkewL, &F->waveL, r, y, nullptr};
+        l.prepared = true;
         wave_sweep(l, ticket, st);
         WaveOp up{kSkewU, &F->waveU, y, x, u};
-        wave_sweep(up, ticket, st);
+        up.prepared = true;
+        wave_sweep(up, ticket + 1, st);
     } else if (F->skew) {
         SkewOp l{kSkewL, &F->planL, r, y, nullptr};
         skew_sweep(l, ticket, st);
@@ -671,14 +674,17 @@ void smooth_ilut(pmg_work_s& W, pmg_csr_s* A, pmg_factor_s* F, double* u, const 
         rr = r;
     }
     // launch counts: our kernels per sweep (sentinel fill, sweep, and the U update pass)
-    if (F->wave) {
+    if (F->wave) {  // one preparation launch for both sweeps, then L, U, and the U update pass
         W.run(fine ? kClsL0 : kClsCoarse, 2, [&] {
+            wave_prepare2(y, x, F->n, W.ticket, W.st);
             WaveOp l{kSkewL, &F->waveL, rr, y, nullptr};
+            l.prepared = true;
             wave_sweep(l, W.ticket, W.st);
         });
-        W.run(fine ? kClsU0 : kClsCoarse, 3, [&] {
+        W.run(fine ? kClsU0 : kClsCoarse, 2, [&] {
             WaveOp up{kSkewU, &F->waveU, y, x, u};
-            wave_sweep(up, W.ticket, W.st);
+            up.prepared = true;
+            wave_sweep(up, W.ticket + 1, W.st);
         });
     } else if (F->skew) {
         W.run(fine ? kClsL0 : kClsCoarse, 2, [&] {
@@ -733,7 +739,7 @@ int smooth(pmg_work_s& W, int l, const double* f, const double* r_known) {
         if (L.A->gs_zero_row >= 0) return PMG_ZERO_DIAG;
         double* uo = w.u[w.cur];
         double* un = w.u[1 - w.cur];
-        W.run(fine ? kClsGS0 : kClsCoarse, (L.A->gs_skew || L.A->gs_wave) ? 3 : 2,
+        W.run(fine ? kClsGS0 : kClsCoarse, L.A->gs_wave ? 2 : L.A->gs_skew ? 3 : 2,
               [&] { gs_apply(L.A, f, uo, un, w.y, W.ticket, W.st); });  // w.y: idle in GS mode
         w.cur = 1 - w.cur;
         return PMG_OK;

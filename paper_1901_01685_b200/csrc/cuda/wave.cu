@@ -674,16 +674,28 @@ __global__ void k_wave_fill(Sell S, const int32_t* __restrict__ nlow, const doub
     item[(ts * 3 + 2) * 32 + lane] = c2;
 }
 
+// Gauss-Seidel pre-pass: the upper sums over the old values; also prepares the sweep (sentinels in
+// its output, claim counter reset) so that a GS sweep is two launches
 __global__ void k_wave_gs_su(Sell S, const int32_t* __restrict__ nlow, const double* __restrict__ old,
-                             double* __restrict__ su) {
+                             double* __restrict__ su, double* __restrict__ out, int* __restrict__ ticket) {
     const int32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v == 0) *ticket = 0;
     if (v >= S.n) return;
+    out[v] = sentinel();
     const int64_t base = S.off[v >> 5];
     const int li = v & 31, len = S.len[v];
     double s = 0.0;
     for (int k = nlow[v]; k < len; ++k)
         s = s + S.val[base + (k >> 1) * 64 + li * 2 + (k & 1)] * old[S.col[base + (k >> 2) * 128 + li * 4 + (k & 3)]];
     su[v] = s;
+}
+
+__global__ void k_wave_prep2(double* __restrict__ y, double* __restrict__ x, int32_t n, int* __restrict__ ticket) {
+    const int32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v == 0) ticket[0] = ticket[1] = 0;
+    if (v >= n) return;
+    y[v] = sentinel();
+    x[v] = sentinel();
 }
 
 __global__ void k_wave_upd(const double* __restrict__ x, double* __restrict__ u, int32_t n) {
@@ -1013,16 +1025,23 @@ void launch_kind(const WavePlan& p, const WaveArgs& a, int grid, cudaStream_t st
 }
 }  // namespace
 
+void wave_prepare2(double* y, double* x, int32_t n, int* ticket, cudaStream_t st) {
+    if (n <= 0) return;
+    k_wave_prep2<<<ceil_div(n, 256), 256, 0, st>>>(y, x, n, ticket);
+    PMG_LAUNCH_CHECK();
+}
+
 void wave_sweep(const WaveOp& op, int* ticket, cudaStream_t st) {
     const WavePlan& p = *op.plan;
     const int32_t n = p.n;
     if (n == 0) return;
     const int nsm = sm_count();
-    fill_sentinel(op.out, n, st);
-    PMG_CUDA(cudaMemsetAsync(ticket, 0, sizeof(int), st));
-    if (op.kind == kSkewGS) {
-        k_wave_gs_su<<<ceil_div(n, 256), 256, 0, st>>>(*op.gsS, op.nlow, op.old, op.su);
+    if (op.kind == kSkewGS) {  // the pre-pass prepares the sweep as well
+        k_wave_gs_su<<<ceil_div(n, 256), 256, 0, st>>>(*op.gsS, op.nlow, op.old, op.su, op.out, ticket);
         PMG_LAUNCH_CHECK();
+    } else if (!op.prepared) {
+        fill_sentinel(op.out, n, st);
+        PMG_CUDA(cudaMemsetAsync(ticket, 0, sizeof(int), st));
     }
     WaveArgs a{};
     a.starts = p.starts;

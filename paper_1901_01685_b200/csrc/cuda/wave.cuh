@@ -53,9 +53,13 @@ struct WaveOp {
     const int32_t* nlow = nullptr;
     const double* old = nullptr;
     double* su = nullptr;
+    bool prepared = false;  // the caller filled `out` with sentinels and zeroed the ticket (wave_prepare2)
 };
 
 void wave_sweep(const WaveOp& op, int* ticket, cudaStream_t st);
+// one launch in place of two sentinel fills and two ticket resets: prepares the outputs of the L
+// and the U sweep of one ILUT application (their claim counters are ticket[0] and ticket[1])
+void wave_prepare2(double* y, double* x, int32_t n, int* ticket, cudaStream_t st);
 
 // diagnostics: one-shot trace of the next sweep, 4 u64 per warp block
 // [globaltimer at step 0, at step 192, at the end, CTA task]
