@@ -4,6 +4,9 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <thread>
 
@@ -317,6 +320,14 @@ static HostCsr make_pattern(const Domain& dom, const Space& rs, const Space& cs)
     return A;
 }
 
+// the host element loops accumulate into the values: start from +0 (parallel first touch)
+static void zero_values(HostCsr& A) {
+    const int64_t nnz = A.nnz(), blk = int64_t(1) << 20;
+    parallel_for((nnz + blk - 1) / blk, [&](int64_t b) {
+        std::fill(A.val.begin() + b * blk, A.val.begin() + std::min(nnz, (b + 1) * blk), 0.0);
+    });
+}
+
 static inline int64_t find_pos(const HostCsr& A, int32_t row, int32_t col) {
     const int32_t* b = A.col.data() + A.rowptr[row];
     const int32_t* e = A.col.data() + A.rowptr[row + 1];
@@ -439,11 +450,21 @@ static void tab_map(const NurbsPatch& g, const Table1D& tx, const Table1D& ty, i
 static HostCsr external_values(const Domain& dom, const Space& rs, const Space& cs, const Cdr* c, int nq, int strip,
                                pmg_asm_values_fn values, const HostCsr* pattern = nullptr,
                                std::vector<double>* lumped = nullptr) {
+    const bool verbose = std::getenv("IGA_VERBOSE") != nullptr;
+    auto t0 = std::chrono::steady_clock::now();
+    auto lap = [&](const char* what) {
+        if (!verbose) return;
+        auto t = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[iga]   %-18s p %d/%d: %.3f s\n", what, rs.p, cs.p, std::chrono::duration<double>(t - t0).count());
+        t0 = t;
+    };
     HostCsr A;
     if (!pattern) {
         A = make_pattern(dom, rs, cs);
         pattern = &A;
     }
+    if (pattern == &A) zero_values(A);  // parallel first touch of the pages the producer copies into
+    lap("pattern");
     if (lumped) lumped->assign(pattern->nrows, 0.0);
     const int nel = rs.nel;
     Basis1D bs;
@@ -491,7 +512,9 @@ static HostCsr external_values(const Domain& dom, const Space& rs, const Space& 
     rq.col_idx = pattern->col.data();
     rq.val = pattern == &A ? A.val.data() : nullptr;
     rq.lumped = lumped ? lumped->data() : nullptr;
+    lap("tables");
     const int rc = values(&rq);
+    lap("values (producer)");
     if (rc == 1) throw GeometryError("nonpositive Jacobian determinant");
     if (rc != 0) throw AssemblyError("external assembler failed (status " + std::to_string(rc) + ")");
     return A;
@@ -510,6 +533,7 @@ HostCsr assemble_operator(const Domain& dom, const Space& sp, const Cdr& c, std:
     const bool ext = values != nullptr;
     if (ext && !rhs) return external_values(dom, sp, sp, &c, nq, p + 1, values);
     HostCsr A = ext ? external_values(dom, sp, sp, &c, nq, p + 1, values) : make_pattern(dom, sp, sp);
+    if (!ext) zero_values(A);
     Basis1D bs;
     bs.build(p, nel, nq);
     if (rhs) rhs->assign(sp.ndof, 0.0);
@@ -657,6 +681,7 @@ static HostCsr assemble_mixed_mass(const Domain& dom, const Space& rs, const Spa
     if (rs.nel != cs.nel) throw AssemblyError("transfer: spaces on different meshes");
     if (values) return external_values(dom, rs, cs, nullptr, std::max(rs.p, cs.p) + 1, std::max(rs.p, cs.p) + 1, values);
     HostCsr A = make_pattern(dom, rs, cs);
+    zero_values(A);
     const int nel = rs.nel, n1 = rs.p + 1, n2 = cs.p + 1, nq = std::max(rs.p, cs.p) + 1;
     const int nr = nel + rs.p, nc = nel + cs.p;
     Basis1D br, bc;

@@ -16,7 +16,9 @@
 #include <cstdint>
 #include <functional>
 #include <stdexcept>
+#include <memory>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../../include/pmg_asm.h"
@@ -28,12 +30,28 @@ struct GeometryError : std::runtime_error { using std::runtime_error::runtime_er
 struct AssemblyError : std::runtime_error { using std::runtime_error::runtime_error; };
 struct ConfigError : std::runtime_error { using std::runtime_error::runtime_error; };
 
+// allocator whose resize() leaves new elements uninitialised: the big CSR arrays are written in
+// full by parallel loops (or by the external producer of the values), so a serial zero fill --
+// and with it the first touch of every page by one thread -- would only cost time
+template <class T>
+struct NoInitAlloc : std::allocator<T> {
+    template <class U>
+    struct rebind {
+        using other = NoInitAlloc<U>;
+    };
+    template <class U, class... Args>
+    void construct(U* p, Args&&... args) {
+        if constexpr (sizeof...(Args) == 0) ::new (static_cast<void*>(p)) U;
+        else ::new (static_cast<void*>(p)) U(std::forward<Args>(args)...);
+    }
+};
+
 // ---- host CSR (int32 offsets/columns, fp64 values) ----
 struct HostCsr {
     int32_t nrows = 0, ncols = 0;
     std::vector<int64_t> rowptr;  // nrows+1 (int64 on the host; device uses int32 where it fits)
-    std::vector<int32_t> col;
-    std::vector<double> val;
+    std::vector<int32_t, NoInitAlloc<int32_t>> col;
+    std::vector<double, NoInitAlloc<double>> val;  // make_pattern leaves it uninitialised
     int64_t nnz() const { return rowptr.empty() ? 0 : rowptr.back(); }
 };
 
