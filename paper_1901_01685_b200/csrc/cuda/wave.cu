@@ -39,6 +39,9 @@ namespace pmg {
 
 namespace {
 
+#ifndef PMG_WAVE_ST
+#define PMG_WAVE_ST 0
+#endif
 #ifndef PMG_WAVE_G
 #define PMG_WAVE_G 32
 #endif
@@ -460,7 +463,15 @@ __global__ void __launch_bounds__(32 * (WMAX + 2)) k_wave(WaveArgs a) {
                 // ring cells are indexed by the step that finalised the value (cells of rows
                 // outside the segment are never read); the output only for real rows
                 if (stage0) rings[rgb + u] = x;
+                // the value other CTAs poll for: PMG_WAVE_ST selects the store flavour (0 plain,
+                // 1 st.global.cg, 2 st.relaxed.gpu)
+#if PMG_WAVE_ST == 1
+                if (stage0 && ix >= 0 && ix < rows) __stcg(outp + ix, x);
+#elif PMG_WAVE_ST == 2
+                if (stage0 && ix >= 0 && ix < rows) st_relaxed_if(outp + ix, x, true);
+#else
                 if (stage0 && ix >= 0 && ix < rows) outp[ix] = x;
+#endif
                 acc = stage0 ? 0.0 : r;
                 if (u % CHK == CHK - 1) st_vol_s(s_me, t + 1);
                 // step t+1's products and last term
