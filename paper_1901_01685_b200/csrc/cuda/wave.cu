@@ -65,6 +65,10 @@ constexpr int WMAX = PMG_WAVE_WMAX;  // sweep warps per CTA
 constexpr int CHK = PMG_WAVE_CHK;
 static_assert(G % CHK == 0, "CHK divides the group");
 constexpr int INF = INT_MAX / 2;
+#ifndef PMG_WAVE_BRIDGE_AHEAD
+#define PMG_WAVE_BRIDGE_AHEAD 64
+#endif
+constexpr int kBridgeAhead = PMG_WAVE_BRIDGE_AHEAD;  // 0: poll every halo row in every iteration
 constexpr unsigned FULL = 0xffffffffu;
 
 struct Layout {
@@ -316,19 +320,28 @@ __global__ void __launch_bounds__(32 * (WMAX + 2)) k_wave(WaveArgs a) {
                 for (int w = 0; w < WMAX; ++w)  // a warp that finished its steps reads no ring cell
                     pr[w] = w < W ? max(ld_acq_s(s_prog + 4 * w), ld_acq_s(sb + ly.rdp + 4 * w)) : INF;
                 double v[MAXD];
+                // the nearest halo row is the one the sweep waits for; an older row is polled only
+                // while its virtual progress is less than kBridgeAhead steps ahead of the nearest
+                // one's (always at the start of a block, then once per ~32 rows): a short loop keeps
+                // the hand-over latency low
+                const bool all = f[0] >= rows[0];
+                const int near_vp = all ? 0 : f[0] + ho[0] + kBridgeAhead;
+                bool polled[MAXD];
 #pragma unroll
                 for (int d = 0; d < MAXD; ++d) {
                     v[d] = sentinel();
+                    polled[d] = f[d] < rows[d] && (d == 0 || all || f[d] + ho[d] < near_vp);
                     int lim = INF;
                     for (int w = 0; w < WMAX; ++w) lim = min(lim, pr[w] >= INF ? INF : pr[w] + hr[w][d]);
                     const int j = f[d] + lane;
-                    if (f[d] < rows[d] && j < rows[d] && j < lim)
+                    if (polled[d] && j < rows[d] && j < lim)
                         v[d] = ld_relaxed_nb(a.out + hb[d] + j);
                 }
                 int vp = INF;
 #pragma unroll
                 for (int d = 0; d < MAXD; ++d) {
-                    if (f[d] < rows[d]) {
+                    if (f[d] < rows[d] && !polled[d]) vp = min(vp, f[d] + ho[d]);
+                    if (polled[d]) {
                         const unsigned ok = __ballot_sync(FULL, !is_sentinel(v[d]));
                         const int cnt = ok == FULL ? 32 : __ffs(~ok) - 1;
                         if (lane < cnt) rings[(DM - 1 - d) * RYS + ((f[d] + lane + sl[d]) & (RY - 1))] = v[d];
