@@ -1,0 +1,74 @@
+// Microbenchmark: one-way latency of handing a double from one SM to another through global memory
+// with the sweeps' protocol -- the producer stores the value (plain / st.global.cg / st.relaxed.gpu),
+// the consumer polls it with ld.relaxed.gpu against a NaN sentinel -- measured as half a ping-pong
+// round trip between two CTAs.  Bounds the cross-CTA hand-over of wave.cu from below.
+// Build: nvcc -arch=sm_100a -O3 handover.cu
+#include <cstdio>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ double ld_relaxed(const double* p) {
+    double v;
+    asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+    return v;
+}
+template <int MODE>
+__device__ __forceinline__ void st(double* p, double v) {
+    if (MODE == 0) *reinterpret_cast<volatile double*>(p) = v;
+    if (MODE == 1) asm volatile("st.global.cg.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+    if (MODE == 2) asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
+// CTA 0 writes a[i], CTA 1 answers in b[i]; one thread each; cells start as NaN
+template <int MODE>
+__global__ void k(double* a, double* b, int n, long long* cyc, unsigned* smid) {
+    if (threadIdx.x != 0) return;
+    unsigned id;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(id));
+    smid[blockIdx.x] = id;
+    long long t0 = clock64();
+    if (blockIdx.x == 0) {
+        for (int i = 0; i < n; ++i) {
+            st<MODE>(a + i, double(i));
+            while (ld_relaxed(b + i) != ld_relaxed(b + i)) {
+            }
+        }
+    } else {
+        for (int i = 0; i < n; ++i) {
+            while (ld_relaxed(a + i) != ld_relaxed(a + i)) {
+            }
+            st<MODE>(b + i, double(i));
+        }
+    }
+    cyc[blockIdx.x] = clock64() - t0;
+}
+
+template <int MODE>
+void run(const char* name) {
+    const int n = 20000;
+    double *a, *b;
+    long long* cyc;
+    unsigned* smid;
+    cudaMalloc(&a, n * 8);
+    cudaMalloc(&b, n * 8);
+    cudaMalloc(&cyc, 16);
+    cudaMalloc(&smid, 8);
+    cudaMemset(a, 0xff, n * 8);
+    cudaMemset(b, 0xff, n * 8);
+    k<MODE><<<2, 32>>>(a, b, n, cyc, smid);
+    long long h[2];
+    unsigned s[2];
+    cudaMemcpy(h, cyc, 16, cudaMemcpyDeviceToHost);
+    cudaMemcpy(s, smid, 8, cudaMemcpyDeviceToHost);
+    int clk = 0;
+    cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+    printf("%-16s SMs %u/%u: round trip %.0f cycles, one way %.0f cycles = %.0f ns at %d MHz\n", name, s[0], s[1],
+           double(h[0]) / n, double(h[0]) / n / 2, double(h[0]) / n / 2 / (clk * 1e-6), clk / 1000);
+    cudaFree(a); cudaFree(b); cudaFree(cyc); cudaFree(smid);
+}
+
+int main() {
+    run<0>("volatile store");
+    run<1>("st.global.cg");
+    run<2>("st.relaxed.gpu");
+    return 0;
+}
