@@ -34,6 +34,12 @@ lag = np.diff(tr[:, 0]) / 1e3
 same = task[1:] == task[:-1]
 print(f"lag between consecutive blocks: same CTA {np.median(lag[same]) if same.any() else float('nan'):.2f} us, "
       f"across CTAs {np.median(lag[~same]) if (~same).any() else float('nan'):.2f} us  (lead {lead} steps)")
+lag_end = np.diff(tr[:, 2]) / 1e3
+print(f"lag between consecutive blocks at their last step: same CTA {np.median(lag_end[same]) if same.any() else float('nan'):.2f} us, "
+      f"across CTAs {np.median(lag_end[~same]) if (~same).any() else float('nan'):.2f} us")
+lag_mid = np.diff(tr[:, 1]) / 1e3
+print(f"lag at step 192: same CTA {np.median(lag_mid[same]) if same.any() else float('nan'):.2f} us, "
+      f"across CTAs {np.median(lag_mid[~same]) if (~same).any() else float('nan'):.2f} us")
 ok = tr[:, 1] > 0
 rate = (tr[ok, 2] - tr[ok, 1]) / 1e3  # us from step 192 to the end
 print("median block duration us", np.median((tr[:, 2] - tr[:, 0]) / 1e3), "median us from step 192 to end", np.median(rate))

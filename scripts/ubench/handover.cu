@@ -42,6 +42,61 @@ __global__ void k(double* a, double* b, int n, long long* cyc, unsigned* smid) {
     cyc[blockIdx.x] = clock64() - t0;
 }
 
+// The same hand-over when the producer does nothing but shared-memory work after the store (as a
+// sweep warp does): the producer stores one value every `gap_ns`, timestamps in shared memory;
+// the consumer polls and timestamps the arrival (%globaltimer on both sides).
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+template <int MODE>
+__global__ void k_oneway(double* a, int n, unsigned gap_ns, unsigned long long* t_send, unsigned long long* t_recv) {
+    __shared__ unsigned long long ts[2048];
+    if (threadIdx.x != 0) return;
+    if (blockIdx.x == 0) {
+        unsigned long long next = gtime() + 20000;
+        for (int i = 0; i < n; ++i) {
+            while (gtime() < next) {
+            }
+            ts[i] = gtime();
+            st<MODE>(a + i, double(i));
+            next += gap_ns;
+        }
+        for (int i = 0; i < n; ++i) t_send[i] = ts[i];
+    } else {
+        for (int i = 0; i < n; ++i) {
+            while (ld_relaxed(a + i) != ld_relaxed(a + i)) {
+            }
+            ts[i] = gtime();
+        }
+        for (int i = 0; i < n; ++i) t_recv[i] = ts[i];
+    }
+}
+template <int MODE>
+void run_oneway(const char* name, unsigned gap_ns) {
+    const int n = 2000;
+    double* a;
+    unsigned long long *ts, *tr;
+    cudaMalloc(&a, n * 8);
+    cudaMalloc(&ts, n * 8);
+    cudaMalloc(&tr, n * 8);
+    cudaMemset(a, 0xff, n * 8);
+    k_oneway<MODE><<<2, 32>>>(a, n, gap_ns, ts, tr);
+    static unsigned long long hs[2000], hr[2000];
+    cudaMemcpy(hs, ts, n * 8, cudaMemcpyDeviceToHost);
+    cudaMemcpy(hr, tr, n * 8, cudaMemcpyDeviceToHost);
+    double sum = 0, mx = 0;
+    for (int i = 100; i < n; ++i) {
+        const double d = double(hr[i]) - double(hs[i]);
+        sum += d;
+        if (d > mx) mx = d;
+    }
+    printf("%-16s one store per %u ns, producer idle otherwise: store -> seen %.0f ns mean, %.0f ns max\n", name, gap_ns,
+           sum / (n - 100), mx);
+    cudaFree(a); cudaFree(ts); cudaFree(tr);
+}
+
 template <int MODE>
 void run(const char* name) {
     const int n = 20000;
@@ -70,5 +125,9 @@ int main() {
     run<0>("volatile store");
     run<1>("st.global.cg");
     run<2>("st.relaxed.gpu");
+    run_oneway<0>("volatile store", 100);
+    run_oneway<0>("volatile store", 2000);
+    run_oneway<2>("st.relaxed.gpu", 100);
+    run_oneway<2>("st.relaxed.gpu", 2000);
     return 0;
 }
