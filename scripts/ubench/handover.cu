@@ -97,6 +97,54 @@ void run_oneway(const char* name, unsigned gap_ns) {
     cudaFree(a); cudaFree(ts); cudaFree(tr);
 }
 
+// ping-pong between block 0 and block `partner` of a grid with one block per SM: the hand-over
+// latency as a function of where the two SMs sit (same TPC / GPC / die or not)
+__global__ void k_pair(double* a, double* b, int n, int partner, long long* cyc, unsigned* smid) {
+    if (threadIdx.x != 0) return;
+    unsigned id;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(id));
+    if (blockIdx.x == 0) {
+        smid[0] = id;
+        long long t0 = clock64();
+        for (int i = 0; i < n; ++i) {
+            st<0>(a + i, double(i));
+            while (ld_relaxed(b + i) != ld_relaxed(b + i)) {
+            }
+        }
+        cyc[0] = clock64() - t0;
+    } else if (int(blockIdx.x) == partner) {
+        smid[1] = id;
+        for (int i = 0; i < n; ++i) {
+            while (ld_relaxed(a + i) != ld_relaxed(a + i)) {
+            }
+            st<0>(b + i, double(i));
+        }
+    }
+}
+void run_pairs() {
+    const int n = 5000;
+    double *a, *b;
+    long long* cyc;
+    unsigned* smid;
+    cudaMalloc(&a, n * 8);
+    cudaMalloc(&b, n * 8);
+    cudaMalloc(&cyc, 16);
+    cudaMalloc(&smid, 8);
+    int nsm = 0;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+    for (int partner = 1; partner < nsm; partner += (partner < 8 ? 1 : 9)) {
+        cudaMemset(a, 0xff, n * 8);
+        cudaMemset(b, 0xff, n * 8);
+        k_pair<<<nsm, 32>>>(a, b, n, partner, cyc, smid);
+        long long h;
+        unsigned s[2];
+        cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
+        cudaMemcpy(s, smid, 8, cudaMemcpyDeviceToHost);
+        printf("pair block 0 / %3d on SMs %3u / %3u: one way %.0f cycles\n", partner, s[0], s[1], double(h) / n / 2);
+    }
+    cudaFree(a); cudaFree(b); cudaFree(cyc); cudaFree(smid);
+}
+
 template <int MODE>
 void run(const char* name) {
     const int n = 20000;
@@ -125,9 +173,8 @@ int main() {
     run<0>("volatile store");
     run<1>("st.global.cg");
     run<2>("st.relaxed.gpu");
-    run_oneway<0>("volatile store", 100);
     run_oneway<0>("volatile store", 2000);
-    run_oneway<2>("st.relaxed.gpu", 100);
     run_oneway<2>("st.relaxed.gpu", 2000);
+    run_pairs();
     return 0;
 }
