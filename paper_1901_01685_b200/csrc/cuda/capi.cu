@@ -1686,7 +1686,7 @@ int pmg_debug_wave_trace(int mode, unsigned long long* out, int cap) {
         return 0;
     }
     if (!g_wave_trace || !out) return 0;
-    const int n = std::min(g_wave_trace_n * 4, cap);
+    const int n = std::min(g_wave_trace_n * 8, cap);
     if (cudaDeviceSynchronize() != cudaSuccess) return -1;
     if (cudaMemcpy(out, g_wave_trace, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
     return g_wave_trace_n;

@@ -129,7 +129,8 @@ struct WaveArgs {
     unsigned sbase;  // shared-window address of the dynamic shared memory the items were built for
     int32_t n, seg, nseg, nblk, ntask, W, dm, ry;
     int32_t slack;   // extra steps of lead over the plan's L_b (see wave_sweep)
-    unsigned long long* trace;  // diagnostics (null: off): per block [start, step 200, end, task]
+    unsigned long long* trace;  // diagnostics (null: off): 8 per block [start, step 192, end, task, bridge: first value
+                                // of the nearest row seen, start published, (sweep) step 32, bridge passes while that row streams in]
     Layout lay;
     int* ticket;
 };
@@ -318,7 +319,9 @@ __global__ void __launch_bounds__(32 * (WMAX + 2)) k_wave(WaveArgs a) {
                 for (int w = 0; w < WMAX; ++w) hr[w][d] = (w < W && d < DM) ? a.hrb[(task * W + w) * MAXD + d] : INF;
             }
             int pub = -INF;
+            int npass = 0;
             for (;;) {
+                if (f[0] > 0 && f[0] < rows[0]) ++npass;  // passes while the nearest row streams in (trace)
                 int pr[WMAX];
                 for (int w = 0; w < WMAX; ++w)  // a warp that finished its steps reads no ring cell
                     pr[w] = w < W ? max(ld_acq_s(s_prog + 4 * w), ld_acq_s(sb + ly.rdp + 4 * w)) : INF;
@@ -352,6 +355,10 @@ __global__ void __launch_bounds__(32 * (WMAX + 2)) k_wave(WaveArgs a) {
                         if (f[d] < rows[d]) vp = min(vp, f[d] + ho[d]);
                     }
                 }
+                if (a.trace && lane == 0 && b0 < a.nblk) {
+                    if (f[0] > 0 && a.trace[b0 * 8 + 4] == 0) a.trace[b0 * 8 + 4] = gtimer();
+                    if (vp >= a.Lb[b0] + a.slack - 1 && a.trace[b0 * 8 + 5] == 0) a.trace[b0 * 8 + 5] = gtimer();
+                }
                 __syncwarp();
                 if (vp > pub) {
                     // PMG_WAVE_BRIDGE_REL=0 publishes with a plain volatile store (as the sweep warps
@@ -366,6 +373,7 @@ __global__ void __launch_bounds__(32 * (WMAX + 2)) k_wave(WaveArgs a) {
                 }
                 if (vp >= INF) break;
             }
+            if (a.trace && lane == 0 && b0 < a.nblk) a.trace[b0 * 8 + 7] = npass;
             continue;
         }
 
@@ -442,13 +450,14 @@ __global__ void __launch_bounds__(32 * (WMAX + 2)) k_wave(WaveArgs a) {
         double* outp = a.out + lo;
         backpressure(0);
         if (a.trace && lane == 0) {
-            a.trace[b * 4 + 0] = gtimer();
-            a.trace[b * 4 + 3] = task;
+            a.trace[b * 8 + 0] = gtimer();
+            a.trace[b * 8 + 3] = task;
         }
         for (int tb = 0; tb < NS; tb += G) {
             const int qg = tb / G;
             const int rgb = myring + (tb & (RY - 1));  // ring cell of step tb (RY is a multiple of G)
-            if (tb == 192 && a.trace && lane == 0) a.trace[b * 4 + 1] = gtimer();
+            if (tb == 192 && a.trace && lane == 0) a.trace[b * 8 + 1] = gtimer();
+            if (tb == 32 && a.trace && lane == 0) a.trace[b * 8 + 6] = gtimer();  // row 0 is final at step 31
 #pragma unroll
             for (int u = 0; u < G; ++u) {
                 const int t = tb + u;
@@ -513,7 +522,7 @@ __global__ void __launch_bounds__(32 * (WMAX + 2)) k_wave(WaveArgs a) {
             refill(qg + NG);
             backpressure(qg + 1);
         }
-        if (a.trace && lane == 0) a.trace[b * 4 + 2] = gtimer();
+        if (a.trace && lane == 0) a.trace[b * 8 + 2] = gtimer();
         // finished: no ring cell is read any more; "done" is published once the predecessor is
         // done (keeps the progress chain valid)
         st_vol_s(sb + ly.rdp + 4 * warp, INF);
@@ -1099,8 +1108,8 @@ void wave_sweep(const WaveOp& op, int* ticket, cudaStream_t st) {
     if (g_wave_trace_on) {  // one-shot trace of the next sweep (diagnostics)
         g_wave_trace_on = false;
         cudaFree(g_wave_trace);
-        PMG_CUDA(cudaMalloc(&g_wave_trace, sizeof(unsigned long long) * 4 * p.nblk));
-        PMG_CUDA(cudaMemsetAsync(g_wave_trace, 0, sizeof(unsigned long long) * 4 * p.nblk, st));
+        PMG_CUDA(cudaMalloc(&g_wave_trace, sizeof(unsigned long long) * 8 * p.nblk));
+        PMG_CUDA(cudaMemsetAsync(g_wave_trace, 0, sizeof(unsigned long long) * 8 * p.nblk, st));
         g_wave_trace_n = p.nblk;
         a.trace = g_wave_trace;
     }
